@@ -1,0 +1,349 @@
+"""bench.py -- FFG + PageRank GTEPS on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c5|c3] [--kind adjacent|hamming]
+
+One step = analyze_landscape on one synthetic search space through the C-ABI:
+FFG build (CSR rows emitted, bit-exact), f_opt, PageRank to tol 1e-10 and
+the C_p curve for p = 0..15 %.  `value` times steps on inputs resident in HBM;
+`e2e` times the same call with host buffers (pinned H2D of the fitness table
+inside the timed region, minima report D2H after it).
+
+GTEPS = E * (iterations + 1) / t_step / 1e9: the FFG build traverses every
+edge once and each PageRank iteration once more.
+
+Multi-GPU (torchrun, one process per GPU): N independent replicas of the
+workload, one per GPU ("scaling": "weak"); value = all edges traversed on all
+ranks / max-over-ranks time.  (Key-range sharding of one space across GPUs
+with a rank-vector exchange is DESIGN.md's next step.)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # C5 "12-param ~1e8 valid", G_iid q = 0.10 seed 5
+    "c5": dict(radix=(8, 8, 8, 6, 6, 6, 4, 4, 4, 4, 2, 2), gen=0, q=0.10, seed=5,
+               desc="synthetic 12-parameter space, 113,246,208 configs (~1.02e8 valid), "
+                    "random fitness table G_iid q=0.10 seed 5"),
+    # C3 "10-param ~1e7 heavy-tailed", G_heavy q = 0 seed 3
+    "c3": dict(radix=(8, 8, 8, 8, 6, 6, 4, 4, 2, 2), gen=1, q=0.0, seed=3,
+               desc="synthetic 10-parameter space, 9,437,184 configs, heavy-tailed "
+                    "runtimes G_heavy seed 3"),
+}
+KIND = {"adjacent": 1, "hamming": 0}
+KERNELS_PER_STEP = 6  # ffg_build, optimum x2, pagerank, cp_partial, cp_final
+DAMPING, TOL, MAX_ITER, P_MAX = 0.85, 1e-10, 100000, 15
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ------------------------------------------------------------ clocks probe --
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.15)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax = float(parts[1])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU legs --
+
+def cpu_sample(wl: dict, kind: int, pr_iters: int = 3):
+    """Bounded CPU sample of the same workload: the first dim-0 slab of the
+    space (all other parameters intact), full FFG build with CSR and minima,
+    `pr_iters` PageRank iterations, C_p.  Oracle port, all host threads."""
+    import oracle as O
+
+    radix = list(wl["radix"])
+    radix[0] = 1
+    n = O.space_size(radix)
+    threads = os.cpu_count() or 1
+    gen = O.gen_iid if wl["gen"] == 0 else O.gen_heavy
+    fit, ok = gen(n, wl["q"], wl["seed"], nthreads=threads)
+    t0 = time.perf_counter()
+    g = O.build_ffg(radix, fit, ok, kind, node_limit=1 << 32, nthreads=threads)
+    pr, it, _ = O.pagerank(g["offsets"], g["targets"], DAMPING, TOL, MAX_ITER,
+                           nthreads=threads, fixed_iters=pr_iters)
+    f_opt, _ = O.optimum(fit, ok)
+    for k in range(P_MAX + 1):
+        O.proportion_of_centrality(g["minima"], fit, pr, f_opt, k / 100.0)
+    dt = time.perf_counter() - t0
+    e = len(g["targets"])
+    return dict(value=e * (pr_iters + 1) / dt / 1e9, seconds=dt, edges=e, nodes=n,
+                threads=threads, iters=pr_iters)
+
+
+def run_reference(args, wl, kind):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_sample(wl, kind)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        s = cpu_sample(wl, kind)
+        vals.append(s["value"])
+        secs += s["seconds"]
+    v = float(np.mean(vals))
+    sample = (f"first dim-0 slab of {args.workload} ({s['nodes']} configs, {s['edges']} edges): "
+              f"FFG build + {s['iters']} PageRank iterations + C_p per step")
+    line = {
+        "metric": "FFG+PageRank GTEPS", "value": v, "unit": "GTEPS", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"]},
+        "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": s["threads"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- GPU leg --
+
+def run_b200(args, wl, kind):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2210_01465_b200 as tk
+
+    radix = wl["radix"]
+    land = tk.Landscape(radix, device=local)
+    land.generate(wl["gen"], wl["q"], wl["seed"] + 0)  # identical replica on every rank
+    stream = torch.cuda.ExternalStream(land.stream, device=torch.device("cuda", local))
+
+    def step():
+        return land.analyze(kind, DAMPING, TOL, MAX_ITER, node_limit=1 << 32,
+                            p_max_percent=P_MAX, emit_csr=True)
+
+    for _ in range(max(3, args.warmup)):
+        s = step()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(local)
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: inputs resident in HBM (> L2: 1 GB fitness + 11 GB FFG state)
+    clocks = ClockSampler(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    clocks.start()
+    ev0.record(stream)
+    sums = []
+    for _ in range(args.steps):
+        sums.append(step())
+    ev1.record(stream)
+    ev1.synchronize()
+    clk = clocks.stop()
+    barrier()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = t_ms / args.steps
+    e = sums[-1].n_edges
+    iters = [x.iterations for x in sums]
+    edges_traversed = sum(e * (it + 1) for it in iters) * world
+    value = edges_traversed / (t_ms / 1e3) / 1e9
+
+    # ---- e2e: the same call from pinned host buffers through the C-ABI
+    fit_h = torch.empty(land.n, dtype=torch.float64, pin_memory=True)
+    ok_h = torch.empty(land.n, dtype=torch.uint8, pin_memory=True)
+    f_np, o_np = land.fitness()
+    fit_h.numpy()[:] = f_np
+    ok_h.numpy()[:] = o_np
+    m = sums[-1].n_minima
+    rep = [torch.empty(m, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    import ctypes as C
+
+    def e2e_step():
+        st = land.L.tk_land_load_dense(land.h, C.c_void_p(fit_h.data_ptr()),
+                                       C.c_void_p(ok_h.data_ptr()), tk._abi.TK_MEM_HOST)
+        assert st == 0, tk._abi.last_error()
+        s2 = step()
+        st = land.L.tk_report_copy_out(land.h, s2.f_opt, C.c_void_p(rep[0].data_ptr()),
+                                       C.c_void_p(rep[1].data_ptr()),
+                                       C.c_void_p(rep[2].data_ptr()),
+                                       C.c_void_p(rep[3].data_ptr()))
+        assert st == 0, tk._abi.last_error()
+        return s2
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    ev0.record(stream)
+    e2e_sums = [e2e_step() for _ in range(args.steps)]
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    t_e2e = max_over_ranks(max(ev0.elapsed_time(ev1), wall_ms))
+    e2e_value = sum(e * (x.iterations + 1) for x in e2e_sums) * world / (t_e2e / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (persistent PageRank, one launch per step)
+    peaks, peak_src = measured_peaks()
+    n = land.n
+    it_last = sums[-1].iterations
+    if land_mode_packed(radix, kind):
+        per_iter, per_pro = 36 * n, 20 * n
+        model = "36 B/node/iteration: packed word 4 + r_old 8 + r_new 8 + c_new 8 + c gather 8"
+    else:
+        per_iter, per_pro = 37 * n, 21 * n
+        model = "37 B/node/iteration: mask 4 + outdeg 1 + r_old 8 + r_new 8 + c_new 8 + c 8"
+    pr_ms = float(np.mean([x.ms_pagerank for x in sums]))
+    pr_bytes = per_pro + per_iter * it_last
+    achieved = pr_bytes / (pr_ms / 1e3) / 1e9
+    ffg_ms = float(np.mean([x.ms_ffg for x in sums]))
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "traffic": None, "kernel": "pagerank_kernel (persistent, cooperative)",
+                "bytes_model": model, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": pr_bytes, "kernel_ms": round(pr_ms, 3),
+                "iterations": it_last}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            c = cpu_sample(wl, kind)
+            cpu = {"value": round(c["value"], 4), "unit": "GTEPS", "cores": c["threads"],
+                   "kind": "port",
+                   "sample": f"oracle/oracle.c (OpenMP) on the first dim-0 slab of "
+                             f"{args.workload}: {c['nodes']} configs, {c['edges']} edges, FFG "
+                             f"+ {c['iters']} PageRank iterations + C_p, {c['seconds']:.1f} s"}
+        ffg_bytes = 22 * n + 4 * e + 4 * sums[-1].n_minima
+        out = {
+            "metric": "FFG+PageRank GTEPS", "value": round(value, 3), "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"],
+                       "nodes": n, "edges": e, "minima": sums[-1].n_minima,
+                       "pagerank_iterations": it_last, "damping": DAMPING, "tol": TOL,
+                       "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (1.0 GB fitness, ~11 GB FFG/PageRank state)"},
+            "s_per_space": round(ms_step / 1e3, 5),
+            "phases_ms": {"ffg_build_kernel": round(ffg_ms, 3),
+                          "pagerank_kernel": round(pr_ms, 3),
+                          "centrality": round(float(np.mean([x.ms_centrality for x in sums])), 3)},
+            "ffg_edges_per_s": round(e / (ffg_ms / 1e3), 1),
+            "ffg_build_gbs": round(ffg_bytes / (ffg_ms / 1e3) / 1e9, 1),
+            "pagerank_gteps": round(e * it_last / (pr_ms / 1e3) / 1e9, 3),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": 9 * n, "d2h_bytes_per_step": 32 * m,
+                    "ms_per_step": round(t_e2e / args.steps, 3)},
+            "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(out))
+    land.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def land_mode_packed(radix, kind) -> bool:
+    dims = sum(1 for m in radix if m >= 2)
+    return kind == 1 and 2 * dims <= 27
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5")
+    ap.add_argument("--kind", choices=sorted(KIND), default="adjacent")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    kind = KIND[args.kind]
+    if args.impl == "reference":
+        return run_reference(args, wl, kind)
+    return run_b200(args, wl, kind)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

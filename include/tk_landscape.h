@@ -1,0 +1,163 @@
+/*
+ * tk_landscape.h -- the C-ABI drop-in boundary for the FFG / PageRank / C_p path.
+ *
+ * Plain C: pointers, sizes, status codes.  No exceptions, no torch or C++ types
+ * cross this boundary.  The C++ drop-in (include/tunekit/landscape.hpp, built on
+ * top of this ABI) rethrows the status codes as the reference's exception types.
+ *
+ * Every entry point names the reference interface it replaces.  Paths are
+ * relative to /root/reference/proj (read-only reference; the declarations there
+ * have no implementation anywhere -- SURVEY.md s0.1):
+ *   landscape.hpp = include/tunekit/landscape.hpp
+ *   cache.hpp     = include/tunekit/cache.hpp
+ *   space.hpp     = include/tunekit/space.hpp
+ *   errors.hpp    = include/tunekit/errors.hpp
+ *
+ * Threading: a tk_land handle is bound to one device and one CUDA stream and is
+ * not thread-safe; use one host thread per handle.  All calls are synchronous
+ * with respect to the host unless stated otherwise.
+ */
+#ifndef TK_LANDSCAPE_H
+#define TK_LANDSCAPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_ABI_VERSION 1
+#define TK_MAX_DIMS 32
+#define TK_MAX_CP 101
+
+/* Status codes.  Mapping onto errors.hpp:10-44:
+ *   TK_EINVAL, TK_ELIMIT -> InvalidArgument   TK_ENOFEAS -> NoFeasiblePoint
+ *   TK_ENOCONV -> NonConvergence              everything else -> Error       */
+enum tk_status {
+    TK_OK = 0,
+    TK_EINVAL = 1,  /* bad argument (errors.hpp:15-17) */
+    TK_ELIMIT = 2,  /* N > node_limit (landscape.hpp:44-45) */
+    TK_ENOFEAS = 3, /* no ok entry (cache.cpp:89-92) */
+    TK_ENOCONV = 4, /* PageRank hit max_iter (errors.hpp:37-42) */
+    TK_EDEGEN = 5,  /* zero minima centrality */
+    TK_ENOMEM = 6,
+    TK_ECUDA = 7,
+    TK_ENCCL = 8,
+    TK_ESTATE = 9   /* call out of order (e.g. pagerank before build) */
+};
+
+/* NeighbourhoodKind, same order as space.hpp:17 */
+enum tk_kind { TK_HAMMING = 0, TK_ADJACENT = 1 };
+/* where a buffer argument lives */
+enum tk_mem { TK_MEM_HOST = 0, TK_MEM_DEVICE = 1 };
+/* device-side synthetic generators (SURVEY.md s8d G_iid / G_heavy), bit-identical
+ * to oracle/oracle.c or_gen_iid / or_gen_heavy */
+enum tk_gen { TK_GEN_IID = 0, TK_GEN_HEAVY = 1 };
+
+typedef struct tk_land tk_land; /* one search space resident on one device */
+
+typedef struct tk_report_summary {
+    uint64_t n_nodes, n_edges, n_minima;
+    double f_opt;         /* cache.hpp:75 optimum() */
+    uint64_t opt_rank;    /* cache.hpp:76 optimum_rank() */
+    int64_t iterations;   /* landscape.hpp:73 pagerank_iterations */
+    double residual;      /* final L1 change */
+    double pagerank_sum;  /* landscape.hpp:74 */
+    int32_t n_cp;         /* p_max_percent + 1 */
+    double c_p[TK_MAX_CP];/* landscape.hpp:72 c_p_curve, pct = 0..p_max */
+    float ms_load, ms_ffg, ms_pagerank, ms_centrality; /* device time per phase */
+} tk_report_summary;
+
+int tk_abi_version(void);
+/* Thread-local message for the last non-OK status on this thread. */
+const char* tk_last_error(void);
+const char* tk_status_name(int status);
+int tk_device_count(int* count);
+
+/* ---------------------------------------------------------------- spaces -- */
+
+/* ParameterSpace shape (space.hpp:26-53): radix[i] = list_size(i), dim 0 most
+ * significant.  N = prod(radix) must be < 2^32 (u32 node ids, landscape.hpp:32). */
+int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** out);
+int tk_land_destroy(tk_land* land);
+int tk_land_info(const tk_land* land, uint64_t* n_nodes, int* device);
+/* The cudaStream_t every kernel of this handle is launched on (for events). */
+void* tk_land_stream(tk_land* land);
+
+/* SearchSpaceCache::mean/ok (cache.hpp:42-48): rank-indexed fitness (failed
+ * entries carry kFailFitness = 1e10, cache.hpp:15) and ok flags.  The cache
+ * must be complete. */
+int tk_land_load_dense(tk_land* land, const double* fitness, const uint8_t* ok, int mem);
+/* Valid set as (key = rank, fitness) pairs: an open-addressing hash table is
+ * built on the device and every absent key becomes a failed node (1e10).
+ * Duplicate keys or keys >= N -> TK_EINVAL. */
+int tk_land_load_sparse(tk_land* land, const uint64_t* keys, const double* fitness,
+                        uint64_t n_valid, int mem);
+/* Same, with configurations as index vectors (row-major int32[n_valid][dims]),
+ * encoded on the device with the mixed-radix rank of space.cpp:72-78. */
+int tk_land_load_configs(tk_land* land, const int32_t* configs, const double* fitness,
+                         uint64_t n_valid, int mem);
+int tk_land_generate(tk_land* land, int gen, double fail_fraction, uint64_t seed);
+int tk_land_copy_fitness(tk_land* land, double* fitness, uint8_t* ok);
+/* Hash lookup of arbitrary keys in the last sparse table: fitness or 1e10. */
+int tk_land_lookup(tk_land* land, const uint64_t* keys, uint64_t n, double* fitness,
+                   uint8_t* found);
+
+/* cache.cpp:55-72,89-98: f_opt = min mean over ok entries, lowest rank on ties. */
+int tk_optimum(tk_land* land, double* f_opt, uint64_t* rank);
+
+/* --------------------------------------------------------------- the FFG -- */
+
+/* build_ffg (landscape.hpp:44-45).  emit_csr = 0 keeps only the compact
+ * per-node neighbour masks (enough for PageRank, C_p and census); 1 also
+ * materialises the out-CSR for tk_ffg_copy_out. */
+int tk_ffg_build(tk_land* land, int kind, uint64_t node_limit, int emit_csr,
+                 uint64_t* n_edges, uint64_t* n_minima);
+/* FitnessFlowGraph fields (landscape.hpp:30-37); caller-allocated host buffers
+ * of N+1, n_edges, N, n_minima elements.  Any pointer may be NULL. */
+int tk_ffg_copy_out(tk_land* land, uint64_t* offsets, uint32_t* targets,
+                    uint8_t* is_sink, uint32_t* minima);
+/* classify_points (landscape.hpp:12-24): strict census on the built FFG's kind.
+ * minima_ranks (host, local_minima entries) may be NULL. */
+int tk_census(tk_land* land, uint64_t* fail_points, uint64_t* local_minima,
+              uint64_t* interior, uint64_t* minima_ranks);
+
+/* ------------------------------------------------------------- PageRank -- */
+
+/* pagerank (landscape.hpp:47-52) on the handle's FFG.  TK_ENOCONV leaves
+ * iterations/residual set (NonConvergence fields, errors.hpp:37-42). */
+int tk_pagerank(tk_land* land, double damping, double tol, int64_t max_iter,
+                int64_t* iterations, double* residual, double* sum);
+int tk_pagerank_copy_out(tk_land* land, double* rank_vector);
+/* proportion_of_centrality (landscape.hpp:56-58) for n_p values of p at once. */
+int tk_centrality(tk_land* land, double f_opt, const double* p, int n_p, double* c_p);
+/* MinimumInfo rows (landscape.hpp:60-65) in ascending rank. */
+int tk_report_copy_out(tk_land* land, double f_opt, uint64_t* ranks, double* fitness,
+                       double* fraction_of_optimum, double* pagerank);
+
+/* analyze_landscape (landscape.hpp:77-79) fused on the device: optimum, FFG,
+ * PageRank, C_p for pct = 0..p_max_percent.  Only the summary leaves the GPU;
+ * minima rows via tk_report_copy_out. */
+int tk_analyze(tk_land* land, int kind, double damping, double tol, int64_t max_iter,
+               uint64_t node_limit, int p_max_percent, int emit_csr,
+               tk_report_summary* out);
+
+/* ---------------------------------------------- free-standing (host CSR) -- */
+
+/* pagerank(const FitnessFlowGraph&) (landscape.hpp:51-52) for an arbitrary
+ * host out-CSR: uploaded, transposed on the device, iterated.  r_out: n doubles. */
+int tk_pagerank_csr(int device, uint64_t n, const uint64_t* offsets,
+                    const uint32_t* targets, double damping, double tol,
+                    int64_t max_iter, double* r_out, int64_t* iterations,
+                    double* residual);
+/* proportion_of_centrality(g, pr, f_opt, p) (landscape.hpp:56-58) over the
+ * minima's fitness and PageRank values (host arrays, ascending rank order). */
+int tk_proportion_of_centrality(int device, uint64_t n_minima, const double* min_fitness,
+                                const double* min_pagerank, double f_opt, double p,
+                                double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TK_LANDSCAPE_H */

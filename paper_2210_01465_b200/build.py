@@ -1,0 +1,70 @@
+"""Build the sm_100a shared library in-tree (it travels to the GPU box with the repo).
+
+    python -m paper_2210_01465_b200.build        # or __graft_entry__.build()
+
+Produces paper_2210_01465_b200/libtk_landscape.so exporting the C-ABI of
+include/tk_landscape.h.  nvcc cross-compiles without a GPU.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libtk_landscape.so")
+SOURCES = ["tk_kernels.cu", "tk_abi.cu"]
+HEADERS = ["tk_internal.cuh", "tk_kernels.cuh"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise FileNotFoundError("nvcc not found")
+
+
+def host_cxx() -> str:
+    # the image exports CC/CXX pointing at a wrapper without the full runtime;
+    # nvcc needs a plain g++ as its host compiler
+    return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+
+
+def flags(extra=()) -> list[str]:
+    return [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+            "-ccbin", host_cxx(), "-Xcompiler", "-fPIC,-ffp-contract=off",
+            "-I", os.path.join(ROOT, "include"), "-I", CSRC, *extra]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "tk_landscape.h"))
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        cmd = [nvcc(), *flags(["-Xptxas", "-v"] if verbose else []), "-c",
+               os.path.join(CSRC, src), "-o", obj]
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    cmd = [nvcc(), *ARCH, "-ccbin", host_cxx(), "-shared", "-o", LIB, *objs]
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,928 @@
+// tk_abi.cu -- the extern "C" boundary declared in include/tk_landscape.h.
+//
+// Host orchestration only: argument checks with the reference's error
+// classes (errors.hpp:10-44 mapped onto tk_status), device buffer ownership,
+// stream ordering, and the few D2H reads the API returns.  All computation is
+// in tk_kernels.cu; there is no host fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "tk_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(e == cudaErrorMemoryAllocation ? TK_ENOMEM : TK_ECUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define TKC(expr)                                              \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);    \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+cudaError_t ensure(DevBuf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.p && b.cap >= bytes) return cudaSuccess;
+    b.release();
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e == cudaSuccess) b.cap = bytes;
+    else b.p = nullptr;
+    return e;
+}
+
+constexpr uint64_t kMaxNodes = 0xFFF00000ull;  // u32 ids with grid-stride headroom
+
+struct PrOut {
+    long long iter;
+    double res;
+    double sum;
+    int parity;
+    int status;
+};
+
+struct Small {  // device-side scalars read back by the host
+    unsigned long long totals[4];
+    double f_opt;
+    unsigned long long rank;
+    int has;
+    int err;
+    int degenerate;
+    int pad;
+    PrOut pr;
+};
+
+}  // namespace
+
+struct tk_land {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<uint32_t> radix_in;
+    std::vector<unsigned long long> strides_in;
+    uint64_t n = 0;
+
+    DevBuf fit, ok;
+    bool loaded = false;
+    DevBuf hkeys, hvals, staging_keys, staging_vals, staging_cfg;
+    uint64_t hcap = 0;
+
+    bool built = false, emitted = false;
+    int kind = TK_ADJACENT, mode = 0;
+    bool wide = false;
+    tk::DevShape shape{};
+    DevBuf pw, inm, odeg, flags, offsets, targets, minima, e_status, m_status, counter;
+    uint64_t n_edges = 0, n_minima = 0, n_strict = 0, n_ok = 0;
+
+    DevBuf r0, r1, c0, c1, part;
+    bool pr_done = false;
+    int pr_parity = 0;
+    long long iterations = 0;
+    double residual = 0.0, pr_sum = 0.0;
+
+    DevBuf small, opt_part, cp_part, cp_out, tmp;
+    Small* hsmall = nullptr;  // pinned mirror
+    cudaEvent_t ev[6] = {};
+    float ms_build = 0.f, ms_pr = 0.f;  // kernel-only device time of the last launch
+    int pr_grid = 0;
+};
+
+namespace {
+
+cudaError_t set_dev(const tk_land* l) { return cudaSetDevice(l->device); }
+
+int check_land(const tk_land* l) {
+    if (!l) return fail(TK_EINVAL, "null tk_land handle");
+    return TK_OK;
+}
+
+tk::DevShape make_shape(const tk_land* l, int kind) {
+    tk::DevShape s{};
+    s.n = static_cast<uint32_t>(l->n);
+    s.kind = kind;
+    int d = 0;
+    for (size_t i = 0; i < l->radix_in.size(); ++i) {
+        if (l->radix_in[i] < 2) continue;  // single-value dims add no neighbours
+        s.radix[d] = l->radix_in[i];
+        s.stride[d] = static_cast<uint32_t>(l->strides_in[i]);
+        ++d;
+    }
+    s.dims = d;
+    int slots = 0;
+    for (int i = 0; i < d; ++i) {
+        s.magic[i] = s.stride[i] == 1 ? 0ull : (~0ull / s.stride[i] + 1ull);
+        s.base[i] = slots;
+        slots += kind == TK_HAMMING ? static_cast<int>(s.radix[i]) - 1 : 2;
+    }
+    s.slots = slots;
+    if (kind == TK_ADJACENT) {
+        // ordered in-slots: v - s_0 < v - s_1 < ... < v - s_{D-1} < v + s_{D-1} < ... < v + s_0
+        for (int j = 0; j < d; ++j) s.nbo[j] = 0u - s.stride[j];
+        for (int j = d; j < 2 * d; ++j) s.nbo[j] = s.stride[2 * d - 1 - j];
+    }
+    return s;
+}
+
+// Undirected neighbour pairs: the edge count when fitness is tie-free and
+// no two failed nodes meet; an upper bound on E always.
+uint64_t max_edges(const tk::DevShape& s) {
+    uint64_t e = 0;
+    for (int i = 0; i < s.dims; ++i) {
+        const uint64_t m = s.radix[i];
+        if (s.kind == TK_HAMMING) e += static_cast<uint64_t>(s.n) / m * (m * (m - 1) / 2);
+        else e += static_cast<uint64_t>(s.n) / m * (m - 1);
+    }
+    return e;
+}
+
+int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
+    if (!l->loaded) return fail(TK_ESTATE, "build_ffg: no fitness table loaded");
+    if (kind != TK_HAMMING && kind != TK_ADJACENT)
+        return fail(TK_EINVAL, "build_ffg: unknown neighbourhood kind");
+    if (l->n > node_limit) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "search space has %llu configurations, above the FFG node limit of %llu; "
+                      "sample the space or raise node_limit",
+                      static_cast<unsigned long long>(l->n),
+                      static_cast<unsigned long long>(node_limit));
+        return fail(TK_ELIMIT, buf);
+    }
+    tk::DevShape s = make_shape(l, kind);
+    if (s.slots > tk::kMaxSlots)
+        return fail(TK_EINVAL, "neighbourhood has " + std::to_string(s.slots) +
+                                   " slots per node; at most 64 are supported");
+    int mode;
+    bool wide = s.slots > 32;
+    if (kind == TK_ADJACENT) mode = s.slots <= tk::kPackedSlots ? tk::MODE_ADJ_PACKED : tk::MODE_ADJ_ORDERED;
+    else mode = tk::MODE_HAM;
+
+    const uint64_t n = l->n;
+    const uint32_t ntiles = static_cast<uint32_t>((n + tk::kBuildThreads - 1) / tk::kBuildThreads);
+    TKC(set_dev(l));
+    if (mode == tk::MODE_ADJ_PACKED) {
+        TKC(ensure(l->pw, n * 4));
+    } else {
+        TKC(ensure(l->inm, n * (wide ? 8 : 4)));
+        TKC(ensure(l->odeg, n));
+    }
+    TKC(ensure(l->flags, n));
+    TKC(ensure(l->minima, n * 4));
+    TKC(ensure(l->e_status, static_cast<size_t>(ntiles) * 8));
+    TKC(ensure(l->m_status, static_cast<size_t>(ntiles) * 8));
+    TKC(ensure(l->counter, 16));
+    if (emit) {
+        TKC(ensure(l->offsets, (n + 1) * 8));
+        TKC(ensure(l->targets, std::max<uint64_t>(1, max_edges(s)) * 4));
+    }
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(l->e_status.p, 0, static_cast<size_t>(ntiles) * 8, l->stream));
+    TKC(cudaMemsetAsync(l->m_status.p, 0, static_cast<size_t>(ntiles) * 8, l->stream));
+    TKC(cudaMemsetAsync(l->counter.p, 0, 16, l->stream));
+    TKC(cudaMemsetAsync(ds->totals, 0, sizeof(ds->totals), l->stream));
+
+    tk::BuildArgs a{};
+    a.fit = l->fit.as<double>();
+    a.ok = l->ok.as<uint8_t>();
+    a.inm = l->inm.p;
+    a.odeg = l->odeg.as<uint8_t>();
+    a.pw = l->pw.as<uint32_t>();
+    a.flags = l->flags.as<uint8_t>();
+    a.offsets = emit ? l->offsets.as<unsigned long long>() : nullptr;
+    a.targets = emit ? l->targets.as<uint32_t>() : nullptr;
+    a.minima = l->minima.as<uint32_t>();
+    a.e_status = l->e_status.as<unsigned long long>();
+    a.m_status = l->m_status.as<unsigned long long>();
+    a.tile_counter = l->counter.as<unsigned int>();
+    a.totals = ds->totals;
+    a.ntiles = ntiles;
+    TKC(cudaEventRecord(l->ev[0], l->stream));
+    TKC(tk::launch_ffg_build(s, mode, wide, emit != 0, a, l->num_sms, l->stream));
+    TKC(cudaEventRecord(l->ev[1], l->stream));
+    TKC(cudaMemcpyAsync(l->hsmall->totals, ds->totals, sizeof(ds->totals),
+                        cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->n_edges = l->hsmall->totals[0];
+    l->n_minima = l->hsmall->totals[1];
+    l->n_strict = l->hsmall->totals[2];
+    l->n_ok = l->hsmall->totals[3];
+    TKC(cudaEventElapsedTime(&l->ms_build, l->ev[0], l->ev[1]));
+    l->shape = s;
+    l->kind = kind;
+    l->mode = mode;
+    l->wide = wide;
+    l->built = true;
+    l->emitted = emit != 0;
+    l->pr_done = false;
+    return TK_OK;
+}
+
+int do_optimum(tk_land* l, double* f_opt, uint64_t* rank) {
+    if (!l->loaded) return fail(TK_ESTATE, "optimum: no fitness table loaded");
+    TKC(set_dev(l));
+    TKC(ensure(l->opt_part, 148 * 4 * 16));
+    Small* ds = l->small.as<Small>();
+    TKC(tk::launch_optimum(l->fit.as<double>(), l->ok.as<uint8_t>(), static_cast<uint32_t>(l->n),
+                           l->opt_part.as<double>(),
+                           reinterpret_cast<unsigned long long*>(l->opt_part.as<double>() + 148 * 4),
+                           &ds->f_opt, &ds->rank, &ds->has, l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->f_opt, &ds->f_opt, 8 + 8 + 4, cudaMemcpyDeviceToHost,
+                        l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    if (!l->hsmall->has) return fail(TK_ENOFEAS, "search space has no ok entry");
+    if (f_opt) *f_opt = l->hsmall->f_opt;
+    if (rank) *rank = l->hsmall->rank;
+    return TK_OK;
+}
+
+int check_pr_args(double d, double tol, int64_t max_iter) {
+    if (!(d >= 0.0 && d <= 1.0)) return fail(TK_EINVAL, "pagerank: damping must lie in [0, 1]");
+    if (!(tol > 0.0)) return fail(TK_EINVAL, "pagerank: tol must be positive");
+    if (max_iter < 1) return fail(TK_EINVAL, "pagerank: max_iter must be >= 1");
+    return TK_OK;
+}
+
+int nonconv(long long it, double res) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "PageRank did not converge: iterations=%lld residual=%.6e", it,
+                  res);
+    return fail(TK_ENOCONV, buf);
+}
+
+// Runs the persistent PageRank kernel over buffers already described by `a`.
+int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool wide,
+                 tk::PrArgs a, DevBuf& part, Small* ds, Small* hs, cudaStream_t stream,
+                 double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
+                 cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr) {
+    (void)device;
+    const int maxg = tk::pagerank_max_grid(mode, wide, num_sms);
+    if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
+    TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
+    const double nd = static_cast<double>(a.n);
+    a.inv_n = 1.0 / nd;
+    a.nd = nd;
+    a.teleport = (1.0 - d) / nd;
+    a.damping = d;
+    a.tol = tol;
+    a.max_iter = max_iter;
+    a.part = part.as<double>();
+    a.out_iter = &ds->pr.iter;
+    a.out_res = &ds->pr.res;
+    a.out_sum = &ds->pr.sum;
+    a.out_parity = &ds->pr.parity;
+    a.out_status = &ds->pr.status;
+    int g = 0;
+    if (e0) TKC(cudaEventRecord(e0, stream));
+    TKC(tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream));
+    if (e1) TKC(cudaEventRecord(e1, stream));
+    TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
+    TKC(cudaStreamSynchronize(stream));
+    if (e0 && e1 && ms) TKC(cudaEventElapsedTime(ms, e0, e1));
+    if (grid) *grid = g;
+    return TK_OK;
+}
+
+int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
+    if (!l->built) return fail(TK_ESTATE, "pagerank: build the FFG first");
+    int st = check_pr_args(d, tol, max_iter);
+    if (st) return st;
+    TKC(set_dev(l));
+    const uint64_t n = l->n;
+    TKC(ensure(l->r0, n * 8));
+    TKC(ensure(l->r1, n * 8));
+    TKC(ensure(l->c0, n * 8));
+    TKC(ensure(l->c1, n * 8));
+    tk::PrArgs a{};
+    a.n = static_cast<uint32_t>(n);
+    a.pw = l->pw.as<uint32_t>();
+    a.inm = l->inm.p;
+    a.odeg = l->odeg.as<uint8_t>();
+    a.r0 = l->r0.as<double>();
+    a.r1 = l->r1.as<double>();
+    a.c0 = l->c0.as<double>();
+    a.c1 = l->c1.as<double>();
+    l->pr_done = false;
+    st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
+                      l->small.as<Small>(), l->hsmall, l->stream, d, tol, max_iter, l->ev[2],
+                      l->ev[3], &l->ms_pr, &l->pr_grid);
+    if (st) return st;
+    const PrOut& o = l->hsmall->pr;
+    l->iterations = o.iter;
+    l->residual = o.res;
+    l->pr_sum = o.sum;
+    l->pr_parity = o.parity;
+    if (o.status != 0) return nonconv(o.iter, o.res);
+    l->pr_done = true;
+    return TK_OK;
+}
+
+const double* pr_result(const tk_land* l) {
+    return l->pr_parity ? l->r1.as<double>() : l->r0.as<double>();
+}
+
+int do_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* c_p) {
+    if (!l->pr_done) return fail(TK_ESTATE, "centrality: run pagerank first");
+    if (n_p < 1 || n_p > TK_MAX_CP) return fail(TK_EINVAL, "centrality: 1..101 values of p");
+    if (l->n_minima == 0) return fail(TK_EDEGEN, "proportion_of_centrality: no local minima");
+    TKC(set_dev(l));
+    TKC(ensure(l->cp_part, static_cast<size_t>(TK_MAX_CP + 1) * tk::kCpBlocks * 8));
+    TKC(ensure(l->cp_out, TK_MAX_CP * 8));
+    Small* ds = l->small.as<Small>();
+    TKC(tk::launch_centrality(l->minima.as<uint32_t>(), l->n_minima, l->fit.as<double>(),
+                              pr_result(l), p, n_p, f_opt, l->cp_part.as<double>(),
+                              l->cp_out.as<double>(), &ds->degenerate, l->stream));
+    TKC(cudaMemcpyAsync(c_p, l->cp_out.p, static_cast<size_t>(n_p) * 8, cudaMemcpyDeviceToHost,
+                        l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->degenerate, &ds->degenerate, 4, cudaMemcpyDeviceToHost,
+                        l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    if (l->hsmall->degenerate)
+        return fail(TK_EDEGEN, "proportion_of_centrality: minima hold zero PageRank mass");
+    return TK_OK;
+}
+
+cudaMemcpyKind h2x(int mem) {
+    return mem == TK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+}
+
+int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const double* dvals,
+                        uint64_t nv) {
+    uint64_t cap = 64;
+    while (cap < 2 * nv) cap <<= 1;
+    TKC(ensure(l->hkeys, cap * 8));
+    TKC(ensure(l->hvals, cap * 8));
+    TKC(ensure(l->fit, l->n * 8));
+    TKC(ensure(l->ok, l->n));
+    l->hcap = cap;
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(l->hkeys.p, 0xFF, cap * 8, l->stream));
+    TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
+    TKC(tk::launch_hash_build(dkeys, dvals, nv, l->n, l->hkeys.as<unsigned long long>(),
+                              l->hvals.as<double>(), cap, &ds->err, l->stream));
+    TKC(tk::launch_hash_densify(l->hkeys.as<unsigned long long>(), l->hvals.as<double>(), cap,
+                                static_cast<uint32_t>(l->n), l->fit.as<double>(),
+                                l->ok.as<uint8_t>(), l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->built = l->pr_done = false;
+    if (l->hsmall->err == 1) {
+        l->loaded = false;
+        return fail(TK_EINVAL, "load: configuration key outside the search space");
+    }
+    if (l->hsmall->err == 2) {
+        l->loaded = false;
+        return fail(TK_EINVAL, "load: duplicate configuration key");
+    }
+    l->loaded = true;
+    return TK_OK;
+}
+
+}  // namespace
+
+// ================================================================ the ABI ==
+
+#define TK_GUARD_BEGIN try {
+#define TK_GUARD_END                                                   \
+    }                                                                  \
+    catch (const std::bad_alloc&) {                                    \
+        return fail(TK_ENOMEM, "host allocation failed");              \
+    }                                                                  \
+    catch (const std::exception& e) {                                  \
+        return fail(TK_EINVAL, e.what());                              \
+    }
+
+extern "C" {
+
+int tk_abi_version(void) { return TK_ABI_VERSION; }
+
+const char* tk_last_error(void) { return g_err.c_str(); }
+
+const char* tk_status_name(int st) {
+    switch (st) {
+        case TK_OK: return "TK_OK";
+        case TK_EINVAL: return "TK_EINVAL";
+        case TK_ELIMIT: return "TK_ELIMIT";
+        case TK_ENOFEAS: return "TK_ENOFEAS";
+        case TK_ENOCONV: return "TK_ENOCONV";
+        case TK_EDEGEN: return "TK_EDEGEN";
+        case TK_ENOMEM: return "TK_ENOMEM";
+        case TK_ECUDA: return "TK_ECUDA";
+        case TK_ENCCL: return "TK_ENCCL";
+        case TK_ESTATE: return "TK_ESTATE";
+        default: return "TK_UNKNOWN";
+    }
+}
+
+int tk_device_count(int* count) {
+    TKC(cudaGetDeviceCount(count));
+    return TK_OK;
+}
+
+int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** out) {
+    TK_GUARD_BEGIN
+    if (!out) return fail(TK_EINVAL, "tk_land_create: null out pointer");
+    *out = nullptr;
+    if (dims == 0 || dims > TK_MAX_DIMS || !radix)
+        return fail(TK_EINVAL, "a space needs 1..32 parameters");
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < dims; ++i) {
+        if (radix[i] == 0) return fail(TK_EINVAL, "parameter with an empty value list");
+        n *= radix[i];
+        if (n > kMaxNodes)
+            return fail(TK_ELIMIT, "search space exceeds the u32 node-id range of the FFG");
+    }
+    int ndev = 0;
+    TKC(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(TK_EINVAL, "no such CUDA device");
+    TKC(cudaSetDevice(device));
+    tk_land* l = new tk_land();
+    l->device = device;
+    l->radix_in.assign(radix, radix + dims);
+    l->strides_in.assign(dims, 1);
+    for (int i = static_cast<int>(dims) - 2; i >= 0; --i)
+        l->strides_in[i] = l->strides_in[i + 1] * radix[i + 1];
+    l->n = n;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e == cudaSuccess) {
+        l->num_sms = prop.multiProcessorCount;
+        if (!prop.cooperativeLaunch) e = cudaErrorNotSupported;
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = ensure(l->small, sizeof(Small));
+    if (e == cudaSuccess) e = cudaMallocHost(&l->hsmall, sizeof(Small));
+    for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&l->ev[i]);
+    if (e != cudaSuccess) {
+        tk_land_destroy(l);
+        return cuda_fail(e, "tk_land_create");
+    }
+    *out = l;
+    return TK_OK;
+    TK_GUARD_END
+}
+
+int tk_land_destroy(tk_land* l) {
+    if (!l) return TK_OK;
+    cudaSetDevice(l->device);
+    if (l->stream) cudaStreamSynchronize(l->stream);
+    DevBuf* bufs[] = {&l->fit, &l->ok, &l->hkeys, &l->hvals, &l->staging_keys, &l->staging_vals,
+                      &l->staging_cfg, &l->pw, &l->inm, &l->odeg, &l->flags, &l->offsets,
+                      &l->targets, &l->minima, &l->e_status, &l->m_status, &l->counter,
+                      &l->r0, &l->r1, &l->c0, &l->c1, &l->part, &l->small, &l->opt_part,
+                      &l->cp_part, &l->cp_out, &l->tmp};
+    for (DevBuf* b : bufs) b->release();
+    if (l->hsmall) cudaFreeHost(l->hsmall);
+    for (auto& ev : l->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (l->stream) cudaStreamDestroy(l->stream);
+    delete l;
+    return TK_OK;
+}
+
+int tk_land_info(const tk_land* l, uint64_t* n_nodes, int* device) {
+    if (int st = check_land(l)) return st;
+    if (n_nodes) *n_nodes = l->n;
+    if (device) *device = l->device;
+    return TK_OK;
+}
+
+void* tk_land_stream(tk_land* l) { return l ? static_cast<void*>(l->stream) : nullptr; }
+
+int tk_land_load_dense(tk_land* l, const double* fitness, const uint8_t* ok, int mem) {
+    if (int st = check_land(l)) return st;
+    if (!fitness || !ok) return fail(TK_EINVAL, "load_dense: null buffer");
+    TKC(set_dev(l));
+    TKC(ensure(l->fit, l->n * 8));
+    TKC(ensure(l->ok, l->n));
+    TKC(cudaMemcpyAsync(l->fit.p, fitness, l->n * 8, h2x(mem), l->stream));
+    TKC(cudaMemcpyAsync(l->ok.p, ok, l->n, h2x(mem), l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->loaded = true;
+    l->built = l->pr_done = false;
+    return TK_OK;
+}
+
+int tk_land_load_sparse(tk_land* l, const uint64_t* keys, const double* fitness,
+                        uint64_t n_valid, int mem) {
+    if (int st = check_land(l)) return st;
+    if ((!keys || !fitness) && n_valid) return fail(TK_EINVAL, "load_sparse: null buffer");
+    TKC(set_dev(l));
+    const unsigned long long* dk = reinterpret_cast<const unsigned long long*>(keys);
+    const double* dv = fitness;
+    if (mem != TK_MEM_DEVICE) {
+        TKC(ensure(l->staging_keys, n_valid * 8));
+        TKC(ensure(l->staging_vals, n_valid * 8));
+        if (n_valid) {
+            TKC(cudaMemcpyAsync(l->staging_keys.p, keys, n_valid * 8, cudaMemcpyHostToDevice,
+                                l->stream));
+            TKC(cudaMemcpyAsync(l->staging_vals.p, fitness, n_valid * 8, cudaMemcpyHostToDevice,
+                                l->stream));
+        }
+        dk = l->staging_keys.as<unsigned long long>();
+        dv = l->staging_vals.as<double>();
+    }
+    return do_load_sparse_keys(l, dk, dv, n_valid);
+}
+
+int tk_land_load_configs(tk_land* l, const int32_t* configs, const double* fitness,
+                         uint64_t n_valid, int mem) {
+    if (int st = check_land(l)) return st;
+    if ((!configs || !fitness) && n_valid) return fail(TK_EINVAL, "load_configs: null buffer");
+    TKC(set_dev(l));
+    const size_t dims = l->radix_in.size();
+    const int32_t* dc = configs;
+    const double* dv = fitness;
+    if (mem != TK_MEM_DEVICE) {
+        TKC(ensure(l->staging_cfg, n_valid * dims * 4));
+        TKC(ensure(l->staging_vals, n_valid * 8));
+        if (n_valid) {
+            TKC(cudaMemcpyAsync(l->staging_cfg.p, configs, n_valid * dims * 4,
+                                cudaMemcpyHostToDevice, l->stream));
+            TKC(cudaMemcpyAsync(l->staging_vals.p, fitness, n_valid * 8, cudaMemcpyHostToDevice,
+                                l->stream));
+        }
+        dc = l->staging_cfg.as<int32_t>();
+        dv = l->staging_vals.as<double>();
+    }
+    TKC(ensure(l->staging_keys, n_valid * 8));
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
+    TKC(tk::launch_encode_configs(dc, n_valid, static_cast<int>(dims), l->radix_in.data(),
+                                  l->strides_in.data(), l->staging_keys.as<unsigned long long>(),
+                                  &ds->err, l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    if (l->hsmall->err)
+        return fail(TK_EINVAL, "load_configs: configuration index outside its value list");
+    return do_load_sparse_keys(l, l->staging_keys.as<unsigned long long>(), dv, n_valid);
+}
+
+int tk_land_generate(tk_land* l, int gen, double fail_fraction, uint64_t seed) {
+    if (int st = check_land(l)) return st;
+    if (gen != TK_GEN_IID && gen != TK_GEN_HEAVY) return fail(TK_EINVAL, "unknown generator");
+    if (!(fail_fraction >= 0.0 && fail_fraction < 1.0))
+        return fail(TK_EINVAL, "fail_fraction must be in [0, 1)");
+    TKC(set_dev(l));
+    TKC(ensure(l->fit, l->n * 8));
+    TKC(ensure(l->ok, l->n));
+    TKC(tk::launch_generate(gen, static_cast<uint32_t>(l->n), fail_fraction, seed,
+                            l->fit.as<double>(), l->ok.as<uint8_t>(), l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->loaded = true;
+    l->built = l->pr_done = false;
+    return TK_OK;
+}
+
+int tk_land_copy_fitness(tk_land* l, double* fitness, uint8_t* ok) {
+    if (int st = check_land(l)) return st;
+    if (!l->loaded) return fail(TK_ESTATE, "copy_fitness: nothing loaded");
+    TKC(set_dev(l));
+    if (fitness)
+        TKC(cudaMemcpyAsync(fitness, l->fit.p, l->n * 8, cudaMemcpyDeviceToHost, l->stream));
+    if (ok) TKC(cudaMemcpyAsync(ok, l->ok.p, l->n, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_land_lookup(tk_land* l, const uint64_t* keys, uint64_t n, double* fitness,
+                   uint8_t* found) {
+    if (int st = check_land(l)) return st;
+    if (!l->hcap) return fail(TK_ESTATE, "lookup: no hash table (load_sparse first)");
+    TKC(set_dev(l));
+    TKC(ensure(l->tmp, n * 17 + 16));
+    unsigned long long* dq = l->tmp.as<unsigned long long>();
+    double* dout = reinterpret_cast<double*>(dq + n);
+    uint8_t* dfound = reinterpret_cast<uint8_t*>(dout + n);
+    TKC(cudaMemcpyAsync(dq, keys, n * 8, cudaMemcpyHostToDevice, l->stream));
+    TKC(tk::launch_hash_lookup(l->hkeys.as<unsigned long long>(), l->hvals.as<double>(), l->hcap,
+                               dq, n, dout, dfound, l->stream));
+    if (fitness) TKC(cudaMemcpyAsync(fitness, dout, n * 8, cudaMemcpyDeviceToHost, l->stream));
+    if (found) TKC(cudaMemcpyAsync(found, dfound, n, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_optimum(tk_land* l, double* f_opt, uint64_t* rank) {
+    if (int st = check_land(l)) return st;
+    return do_optimum(l, f_opt, rank);
+}
+
+int tk_ffg_build(tk_land* l, int kind, uint64_t node_limit, int emit_csr, uint64_t* n_edges,
+                 uint64_t* n_minima) {
+    if (int st = check_land(l)) return st;
+    TK_GUARD_BEGIN
+    int st = do_build(l, kind, node_limit, emit_csr);
+    if (st) return st;
+    if (n_edges) *n_edges = l->n_edges;
+    if (n_minima) *n_minima = l->n_minima;
+    return TK_OK;
+    TK_GUARD_END
+}
+
+int tk_ffg_copy_out(tk_land* l, uint64_t* offsets, uint32_t* targets, uint8_t* is_sink,
+                    uint32_t* minima) {
+    if (int st = check_land(l)) return st;
+    if (!l->built) return fail(TK_ESTATE, "copy_out: build the FFG first");
+    TKC(set_dev(l));
+    if ((offsets || targets) && !l->emitted) {
+        const bool pr = l->pr_done;
+        int st = do_build(l, l->kind, ~0ull, 1);  // re-emit the CSR rows (same graph)
+        if (st) return st;
+        l->pr_done = pr;
+    }
+    if (offsets)
+        TKC(cudaMemcpyAsync(offsets, l->offsets.p, (l->n + 1) * 8, cudaMemcpyDeviceToHost,
+                            l->stream));
+    if (targets && l->n_edges)
+        TKC(cudaMemcpyAsync(targets, l->targets.p, l->n_edges * 4, cudaMemcpyDeviceToHost,
+                            l->stream));
+    if (minima && l->n_minima)
+        TKC(cudaMemcpyAsync(minima, l->minima.p, l->n_minima * 4, cudaMemcpyDeviceToHost,
+                            l->stream));
+    if (is_sink) {
+        TKC(ensure(l->tmp, l->n));
+        TKC(tk::launch_flags_to_sink(l->flags.as<uint8_t>(), static_cast<uint32_t>(l->n),
+                                     l->tmp.as<uint8_t>(), l->stream));
+        TKC(cudaMemcpyAsync(is_sink, l->tmp.p, l->n, cudaMemcpyDeviceToHost, l->stream));
+    }
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_census(tk_land* l, uint64_t* fail_points, uint64_t* local_minima, uint64_t* interior,
+              uint64_t* minima_ranks) {
+    if (int st = check_land(l)) return st;
+    if (!l->built) return fail(TK_ESTATE, "census: build the FFG first");
+    TKC(set_dev(l));
+    // strict minima (flag bit2) compacted in ascending rank with a look-back scan
+    const uint32_t ntiles = static_cast<uint32_t>((l->n + 255) / 256);
+    if (minima_ranks && l->n_strict) {
+        TKC(ensure(l->tmp, l->n_strict * 8));
+        TKC(cudaMemsetAsync(l->e_status.p, 0, static_cast<size_t>(ntiles) * 8, l->stream));
+        TKC(cudaMemsetAsync(l->counter.p, 0, 16, l->stream));
+        TKC(tk::launch_compact_flags(l->flags.as<uint8_t>(), 4, static_cast<uint32_t>(l->n),
+                                     l->tmp.as<unsigned long long>(),
+                                     l->e_status.as<unsigned long long>(),
+                                     l->counter.as<unsigned int>(), ntiles, l->num_sms,
+                                     l->stream));
+        TKC(cudaMemcpyAsync(minima_ranks, l->tmp.p, l->n_strict * 8, cudaMemcpyDeviceToHost,
+                            l->stream));
+        TKC(cudaStreamSynchronize(l->stream));
+    }
+    if (fail_points) *fail_points = l->n - l->n_ok;
+    if (local_minima) *local_minima = l->n_strict;
+    if (interior) *interior = l->n_ok - l->n_strict;
+    return TK_OK;
+}
+
+int tk_pagerank(tk_land* l, double damping, double tol, int64_t max_iter, int64_t* iterations,
+                double* residual, double* sum) {
+    if (int st = check_land(l)) return st;
+    int st = do_pagerank(l, damping, tol, max_iter);
+    if (iterations) *iterations = l->iterations;
+    if (residual) *residual = l->residual;
+    if (sum) *sum = l->pr_sum;
+    return st;
+}
+
+int tk_pagerank_copy_out(tk_land* l, double* r) {
+    if (int st = check_land(l)) return st;
+    if (!l->pr_done) return fail(TK_ESTATE, "pagerank_copy_out: no converged PageRank");
+    TKC(set_dev(l));
+    TKC(cudaMemcpyAsync(r, pr_result(l), l->n * 8, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* c_p) {
+    if (int st = check_land(l)) return st;
+    if (!p || !c_p) return fail(TK_EINVAL, "centrality: null buffer");
+    return do_centrality(l, f_opt, p, n_p, c_p);
+}
+
+int tk_report_copy_out(tk_land* l, double f_opt, uint64_t* ranks, double* fitness,
+                       double* fraction, double* pagerank) {
+    if (int st = check_land(l)) return st;
+    if (!l->pr_done) return fail(TK_ESTATE, "report: run pagerank first");
+    const uint64_t m = l->n_minima;
+    if (!m) return TK_OK;
+    TKC(set_dev(l));
+    TKC(ensure(l->tmp, m * 32));
+    unsigned long long* dr = l->tmp.as<unsigned long long>();
+    double* df = reinterpret_cast<double*>(dr + m);
+    double* dfr = df + m;
+    double* dp = dfr + m;
+    TKC(tk::launch_report(l->minima.as<uint32_t>(), m, l->fit.as<double>(), pr_result(l), f_opt,
+                          dr, df, dfr, dp, l->stream));
+    if (ranks) TKC(cudaMemcpyAsync(ranks, dr, m * 8, cudaMemcpyDeviceToHost, l->stream));
+    if (fitness) TKC(cudaMemcpyAsync(fitness, df, m * 8, cudaMemcpyDeviceToHost, l->stream));
+    if (fraction) TKC(cudaMemcpyAsync(fraction, dfr, m * 8, cudaMemcpyDeviceToHost, l->stream));
+    if (pagerank) TKC(cudaMemcpyAsync(pagerank, dp, m * 8, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_analyze(tk_land* l, int kind, double damping, double tol, int64_t max_iter,
+               uint64_t node_limit, int p_max_percent, int emit_csr, tk_report_summary* out) {
+    if (int st = check_land(l)) return st;
+    if (!out) return fail(TK_EINVAL, "analyze: null summary");
+    if (p_max_percent < 0 || p_max_percent >= TK_MAX_CP)
+        return fail(TK_EINVAL, "analyze: p_max_percent must be in [0, 100]");
+    int st = check_pr_args(damping, tol, max_iter);
+    if (st) return st;
+    TK_GUARD_BEGIN
+    std::memset(out, 0, sizeof(*out));
+    TKC(set_dev(l));
+    st = do_build(l, kind, node_limit, emit_csr);
+    if (st) return st;
+    double f_opt = 0.0;
+    uint64_t orank = 0;
+    st = do_optimum(l, &f_opt, &orank);
+    if (st) return st;
+    st = do_pagerank(l, damping, tol, max_iter);
+    out->iterations = l->iterations;
+    out->residual = l->residual;
+    if (st) return st;
+    TKC(cudaEventRecord(l->ev[4], l->stream));
+    double ps[TK_MAX_CP];
+    const int np = p_max_percent + 1;
+    for (int k = 0; k < np; ++k) ps[k] = k / 100.0;
+    st = do_centrality(l, f_opt, ps, np, out->c_p);
+    if (st) return st;
+    TKC(cudaEventRecord(l->ev[5], l->stream));
+    TKC(cudaEventSynchronize(l->ev[5]));
+    out->n_nodes = l->n;
+    out->n_edges = l->n_edges;
+    out->n_minima = l->n_minima;
+    out->f_opt = f_opt;
+    out->opt_rank = orank;
+    out->pagerank_sum = l->pr_sum;
+    out->n_cp = np;
+    out->ms_load = 0.f;
+    out->ms_ffg = l->ms_build;
+    out->ms_pagerank = l->ms_pr;
+    TKC(cudaEventElapsedTime(&out->ms_centrality, l->ev[4], l->ev[5]));
+    return TK_OK;
+    TK_GUARD_END
+}
+
+int tk_pagerank_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* targets,
+                    double damping, double tol, int64_t max_iter, double* r_out,
+                    int64_t* iterations, double* residual) {
+    if (n == 0) return fail(TK_EINVAL, "pagerank: empty graph");
+    if (n > kMaxNodes) return fail(TK_ELIMIT, "pagerank: graph exceeds u32 node ids");
+    if (!offsets || !r_out) return fail(TK_EINVAL, "pagerank: null buffer");
+    int st = check_pr_args(damping, tol, max_iter);
+    if (st) return st;
+    const uint64_t e = offsets[n];
+    if (e && !targets) return fail(TK_EINVAL, "pagerank: null targets");
+    for (uint64_t i = 0; i < n; ++i)
+        if (offsets[i] > offsets[i + 1]) return fail(TK_EINVAL, "pagerank: offsets not monotone");
+    TK_GUARD_BEGIN
+    int ndev = 0;
+    TKC(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(TK_EINVAL, "no such CUDA device");
+    TKC(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TKC(cudaGetDeviceProperties(&prop, device));
+    cudaStream_t stream;
+    TKC(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    DevBuf off, tg, odeg, indeg, in_off, src, status, counter, r0, r1, c0, c1, part, small;
+    Small* hs = nullptr;
+    auto cleanup = [&]() {
+        cudaStreamSynchronize(stream);
+        for (DevBuf* b : {&off, &tg, &odeg, &indeg, &in_off, &src, &status, &counter, &r0, &r1,
+                          &c0, &c1, &part, &small})
+            b->release();
+        if (hs) cudaFreeHost(hs);
+        cudaStreamDestroy(stream);
+    };
+    auto run = [&]() -> int {
+        const uint32_t nn = static_cast<uint32_t>(n);
+        const uint32_t ntiles = static_cast<uint32_t>((n + 255) / 256);
+        TKC(ensure(off, (n + 1) * 8));
+        TKC(ensure(tg, std::max<uint64_t>(e, 1) * 4));
+        TKC(ensure(odeg, n * 4));
+        TKC(ensure(indeg, n * 4));
+        TKC(ensure(in_off, (n + 1) * 8));
+        TKC(ensure(src, std::max<uint64_t>(e, 1) * 4));
+        TKC(ensure(status, static_cast<size_t>(ntiles) * 8));
+        TKC(ensure(counter, 16));
+        TKC(ensure(r0, n * 8));
+        TKC(ensure(r1, n * 8));
+        TKC(ensure(c0, n * 8));
+        TKC(ensure(c1, n * 8));
+        TKC(ensure(small, sizeof(Small)));
+        TKC(cudaMallocHost(&hs, sizeof(Small)));
+        TKC(cudaMemcpyAsync(off.p, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, stream));
+        if (e) TKC(cudaMemcpyAsync(tg.p, targets, e * 4, cudaMemcpyHostToDevice, stream));
+        TKC(cudaMemsetAsync(indeg.p, 0, n * 4, stream));
+        TKC(cudaMemsetAsync(status.p, 0, static_cast<size_t>(ntiles) * 8, stream));
+        TKC(cudaMemsetAsync(counter.p, 0, 16, stream));
+        Small* ds = small.as<Small>();
+        TKC(cudaMemsetAsync(&ds->err, 0, 4, stream));
+        // target range check happens on the host: cheap, and keeps the kernel simple
+        for (uint64_t i = 0; i < e; ++i)
+            if (targets[i] >= n) return fail(TK_EINVAL, "pagerank: edge target out of range");
+        TKC(tk::launch_csr_prepare(nn, off.as<unsigned long long>(), tg.as<uint32_t>(), e,
+                                   odeg.as<uint32_t>(), indeg.as<uint32_t>(), stream));
+        TKC(tk::launch_exclusive_scan_u32(indeg.as<uint32_t>(), nn, in_off.as<unsigned long long>(),
+                                          status.as<unsigned long long>(),
+                                          counter.as<unsigned int>(), ntiles,
+                                          prop.multiProcessorCount, stream));
+        TKC(cudaMemsetAsync(indeg.p, 0, n * 4, stream));  // reuse as scatter cursor
+        TKC(tk::launch_csr_scatter(nn, off.as<unsigned long long>(), tg.as<uint32_t>(),
+                                   in_off.as<unsigned long long>(), indeg.as<uint32_t>(),
+                                   src.as<uint32_t>(), stream));
+        TKC(tk::launch_csr_sort_rows(nn, in_off.as<unsigned long long>(), src.as<uint32_t>(),
+                                     stream));
+        tk::DevShape s{};
+        s.n = nn;
+        tk::PrArgs a{};
+        a.n = nn;
+        a.in_off = in_off.as<unsigned long long>();
+        a.src = src.as<uint32_t>();
+        a.odeg32 = odeg.as<uint32_t>();
+        a.r0 = r0.as<double>();
+        a.r1 = r1.as<double>();
+        a.c0 = c0.as<double>();
+        a.c1 = c1.as<double>();
+        int rs = run_pagerank(device, prop.multiProcessorCount, s, tk::MODE_CSR, false, a, part,
+                              ds, hs, stream, damping, tol, max_iter);
+        if (rs) return rs;
+        if (iterations) *iterations = hs->pr.iter;
+        if (residual) *residual = hs->pr.res;
+        if (hs->pr.status != 0) return nonconv(hs->pr.iter, hs->pr.res);
+        TKC(cudaMemcpyAsync(r_out, hs->pr.parity ? r1.p : r0.p, n * 8, cudaMemcpyDeviceToHost,
+                            stream));
+        TKC(cudaStreamSynchronize(stream));
+        return TK_OK;
+    };
+    st = run();
+    cleanup();
+    return st;
+    TK_GUARD_END
+}
+
+int tk_proportion_of_centrality(int device, uint64_t n_minima, const double* min_fitness,
+                                const double* min_pagerank, double f_opt, double p,
+                                double* out) {
+    if (!out) return fail(TK_EINVAL, "proportion_of_centrality: null out");
+    if (n_minima == 0) return fail(TK_EDEGEN, "proportion_of_centrality: no local minima");
+    if (!min_fitness || !min_pagerank) return fail(TK_EINVAL, "proportion_of_centrality: null buffer");
+    TKC(cudaSetDevice(device));
+    cudaStream_t stream;
+    TKC(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    DevBuf f, r, part, cp, small;
+    int deg = 0;
+    auto run = [&]() -> int {
+        TKC(ensure(f, n_minima * 8));
+        TKC(ensure(r, n_minima * 8));
+        TKC(ensure(part, 2 * tk::kCpBlocks * 8));
+        TKC(ensure(cp, 8));
+        TKC(ensure(small, sizeof(Small)));
+        TKC(cudaMemcpyAsync(f.p, min_fitness, n_minima * 8, cudaMemcpyHostToDevice, stream));
+        TKC(cudaMemcpyAsync(r.p, min_pagerank, n_minima * 8, cudaMemcpyHostToDevice, stream));
+        Small* ds = small.as<Small>();
+        TKC(tk::launch_centrality(nullptr, n_minima, f.as<double>(), r.as<double>(), &p, 1, f_opt,
+                                  part.as<double>(), cp.as<double>(), &ds->degenerate, stream));
+        TKC(cudaMemcpyAsync(out, cp.p, 8, cudaMemcpyDeviceToHost, stream));
+        TKC(cudaMemcpyAsync(&deg, &ds->degenerate, 4, cudaMemcpyDeviceToHost, stream));
+        TKC(cudaStreamSynchronize(stream));
+        if (deg) return fail(TK_EDEGEN, "proportion_of_centrality: minima hold zero PageRank mass");
+        return TK_OK;
+    };
+    int st = run();
+    cudaStreamSynchronize(stream);
+    for (DevBuf* b : {&f, &r, &part, &cp, &small}) b->release();
+    cudaStreamDestroy(stream);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// tk_kernels.cuh -- host-side launch wrappers for the sm_100a kernels.
+// Every wrapper enqueues on `stream` and returns a cudaError_t; none blocks.
+#pragma once
+
+#include "tk_internal.cuh"
+
+namespace tk {
+
+// ---- ingestion -------------------------------------------------------------
+cudaError_t launch_generate(int gen, uint32_t n, double q, uint64_t seed, double* fit,
+                            uint8_t* ok, cudaStream_t stream);
+cudaError_t launch_encode_configs(const int32_t* configs, uint64_t n_valid, int dims_in,
+                                  const uint32_t* radix_in_host,
+                                  const unsigned long long* strides_in_host,
+                                  unsigned long long* keys_out, int* err_flag,
+                                  cudaStream_t stream);
+cudaError_t launch_hash_build(const unsigned long long* keys, const double* vals,
+                              uint64_t n_valid, uint64_t n_nodes,
+                              unsigned long long* hkeys, double* hvals, uint64_t cap,
+                              int* err_flag, cudaStream_t stream);
+cudaError_t launch_hash_densify(const unsigned long long* hkeys, const double* hvals,
+                                uint64_t cap, uint32_t n, double* fit, uint8_t* ok,
+                                cudaStream_t stream);
+cudaError_t launch_hash_lookup(const unsigned long long* hkeys, const double* hvals,
+                               uint64_t cap, const unsigned long long* q, uint64_t nq,
+                               double* out, uint8_t* found, cudaStream_t stream);
+cudaError_t launch_optimum(const double* fit, const uint8_t* ok, uint32_t n,
+                           double* part_f, unsigned long long* part_r, double* f_opt,
+                           unsigned long long* rank, int* has, cudaStream_t stream);
+
+// ---- FFG ---------------------------------------------------------------------
+struct BuildArgs {
+    const double* fit;
+    const uint8_t* ok;
+    void* inm;            // in-mask (u32 or u64 per node) -- not packed mode
+    uint8_t* odeg;        // out-degree -- not packed mode
+    uint32_t* pw;         // packed word -- packed mode
+    uint8_t* flags;       // bit0 sink, bit1 ok&&sink, bit2 strict minimum, bit3 ok
+    unsigned long long* offsets;  // N+1 (emit)
+    uint32_t* targets;            // E (emit)
+    uint32_t* minima;             // M
+    unsigned long long* e_status; // per tile
+    unsigned long long* m_status; // per tile
+    unsigned int* tile_counter;
+    unsigned long long* totals;   // [0] E, [1] M, [2] strict minima, [3] ok nodes
+    uint32_t ntiles;
+};
+constexpr int kBuildThreads = 256;
+cudaError_t launch_ffg_build(const DevShape& s, int mode, bool wide, bool emit,
+                             const BuildArgs& a, int num_sms, cudaStream_t stream);
+
+// flags & mask != 0 -> ascending u64 ranks (generic compaction, look-back)
+cudaError_t launch_compact_flags(const uint8_t* flags, uint8_t mask, uint32_t n,
+                                 unsigned long long* out, unsigned long long* status,
+                                 unsigned int* tile_counter, uint32_t ntiles,
+                                 int num_sms, cudaStream_t stream);
+cudaError_t launch_flags_to_sink(const uint8_t* flags, uint32_t n, uint8_t* is_sink,
+                                 cudaStream_t stream);
+
+// ---- CSR transpose (tk_pagerank_csr) -------------------------------------
+cudaError_t launch_csr_prepare(uint32_t n, const unsigned long long* offsets,
+                               const uint32_t* targets, uint64_t e, uint32_t* odeg32,
+                               uint32_t* indeg, cudaStream_t stream);
+cudaError_t launch_exclusive_scan_u32(const uint32_t* in, uint32_t n,
+                                      unsigned long long* out /* n+1 */,
+                                      unsigned long long* status, unsigned int* tile_counter,
+                                      uint32_t ntiles, int num_sms, cudaStream_t stream);
+cudaError_t launch_csr_scatter(uint32_t n, const unsigned long long* offsets,
+                               const uint32_t* targets, const unsigned long long* in_off,
+                               uint32_t* cursor, uint32_t* src, cudaStream_t stream);
+cudaError_t launch_csr_sort_rows(uint32_t n, const unsigned long long* in_off, uint32_t* src,
+                                 cudaStream_t stream);
+
+// ---- PageRank ----------------------------------------------------------------
+struct PrArgs {
+    uint32_t n;
+    double inv_n;      // 1.0 / N
+    double nd;         // (double) N
+    double teleport;   // (1 - d) / N
+    double damping;
+    double tol;
+    long long max_iter;
+    const uint32_t* pw;            // MODE_ADJ_PACKED
+    const void* inm;               // MODE_ADJ_ORDERED / MODE_HAM
+    const uint8_t* odeg;           // idem
+    const unsigned long long* in_off;  // MODE_CSR
+    const uint32_t* src;               // MODE_CSR
+    const uint32_t* odeg32;            // MODE_CSR
+    double* r0;
+    double* r1;
+    double* c0;
+    double* c1;
+    double* part;                  // [2][grid][3]
+    long long* out_iter;
+    double* out_res;
+    double* out_sum;
+    int* out_parity;               // buffer index holding the result
+    int* out_status;               // 0 converged, 1 max_iter
+};
+constexpr int kPrThreads = 256;
+// grid_out receives the cooperative grid size used.
+cudaError_t launch_pagerank(const DevShape& s, int mode, bool wide, const PrArgs& a,
+                            int num_sms, int* grid_out, cudaStream_t stream);
+int pagerank_max_grid(int mode, bool wide, int num_sms);
+
+// ---- C_p and report -------------------------------------------------------
+constexpr int kCpBlocks = 148;
+// minima == nullptr: fit/r are already per-minimum arrays of length m.
+cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* fit,
+                              const double* r, const double* p, int n_p, double f_opt,
+                              double* part, double* c_p_out, int* degenerate,
+                              cudaStream_t stream);
+cudaError_t launch_report(const uint32_t* minima, uint64_t m, const double* fit,
+                          const double* r, double f_opt, unsigned long long* ranks,
+                          double* fitness, double* fraction, double* pr,
+                          cudaStream_t stream);
+cudaError_t launch_gather_values(const uint32_t* idx, uint64_t m, const double* src,
+                                 double* dst, cudaStream_t stream);
+
+}  // namespace tk

@@ -1,0 +1,408 @@
+"""Host-side mirror of the reference's landscape interface over the C-ABI.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/tunekit/landscape.hpp (declarations only in the
+reference) so tests read like the reference's own would:
+
+  classify_points        landscape.hpp:15-24     -> PointCensus
+  build_ffg              landscape.hpp:30-45     -> FitnessFlowGraph
+  pagerank               landscape.hpp:47-52     -> numpy f64[N]
+  proportion_of_centrality  landscape.hpp:54-58  -> float
+  analyze_landscape      landscape.hpp:60-79     -> CentralityReport
+  minima_fraction_report landscape.hpp:87-94     -> MinimaFractionReport
+
+Errors map onto the reference's classes (errors.hpp:10-44).  Every call runs
+on the GPU through libtk_landscape.so; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import TK_ADJACENT, TK_HAMMING  # noqa: F401  (re-export)
+
+HAMMING, ADJACENT = TK_HAMMING, TK_ADJACENT
+K_FAIL_FITNESS = 1.0e10  # cache.hpp:15
+
+
+# ------------------------------------------------------------------ errors --
+
+class Error(RuntimeError):
+    """errors.hpp:10-13"""
+
+
+class InvalidArgument(Error):
+    """errors.hpp:15-19"""
+
+
+class NoFeasiblePoint(Error):
+    """errors.hpp:32-35"""
+
+
+class NonConvergence(Error):
+    """errors.hpp:37-42"""
+
+    def __init__(self, what: str, iterations: int, residual: float):
+        super().__init__(what)
+        self.iterations = iterations
+        self.residual = residual
+
+
+def _check(st: int, iterations: int = 0, residual: float = 0.0) -> None:
+    if st == _abi.TK_OK:
+        return
+    msg = _abi.last_error()
+    if st in (_abi.TK_EINVAL, _abi.TK_ELIMIT):
+        raise InvalidArgument(msg)
+    if st == _abi.TK_ENOFEAS:
+        raise NoFeasiblePoint(msg)
+    if st == _abi.TK_ENOCONV:
+        raise NonConvergence(msg, iterations, residual)
+    raise Error(f"{_abi.load().tk_status_name(st).decode()}: {msg}")
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def neighbourhood_from_string(s: str) -> int:
+    """space.cpp:12-17"""
+    if s in ("hamming", "Hamming"):
+        return HAMMING
+    if s in ("adjacent", "Adjacent"):
+        return ADJACENT
+    raise InvalidArgument(f"unknown neighbourhood: {s} (expected hamming or adjacent)")
+
+
+# ------------------------------------------------------------ data types --
+
+class SearchSpaceCache:
+    """The slice of cache.hpp:23-82 the landscape path reads: the space shape
+    (list sizes, dim 0 most significant) and the rank-indexed mean/ok tables."""
+
+    def __init__(self, radix, mean, ok, kernel: str = "", device: str = ""):
+        self.radix = [int(m) for m in radix]
+        self.mean_ = np.ascontiguousarray(mean, np.float64)
+        self.ok_ = np.ascontiguousarray(ok, np.uint8)
+        n = int(np.prod(self.radix, dtype=np.uint64)) if self.radix else 1
+        if self.mean_.shape != (n,) or self.ok_.shape != (n,):
+            raise InvalidArgument("cache tables must hold one entry per configuration")
+        self.kernel, self.device = kernel, device
+
+    def size(self) -> int:
+        return self.mean_.shape[0]
+
+    def mean(self, rank: int) -> float:
+        return float(self.mean_[rank])
+
+    def ok(self, rank: int) -> bool:
+        return bool(self.ok_[rank])
+
+    def ok_count(self) -> int:
+        return int(self.ok_.sum())
+
+    def _opt(self):
+        with Landscape(self.radix) as land:
+            land.load_dense(self.mean_, self.ok_)
+            return land.optimum()
+
+    def optimum(self) -> float:
+        """cache.cpp:89-93 (computed on the device)."""
+        return self._opt()[0]
+
+    def optimum_rank(self) -> int:
+        return self._opt()[1]
+
+
+@dataclass
+class PointCensus:  # landscape.hpp:15-22
+    kind: int = ADJACENT
+    total: int = 0
+    fail_points: int = 0
+    local_minima: int = 0
+    interior: int = 0
+    minima_ranks: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+
+
+@dataclass
+class FitnessFlowGraph:  # landscape.hpp:30-42
+    kind: int
+    node_count: int
+    offsets: np.ndarray
+    targets: np.ndarray
+    fitness: np.ndarray
+    is_sink: np.ndarray
+    minima: np.ndarray
+
+    def out_degree(self, u: int) -> int:
+        return int(self.offsets[u + 1] - self.offsets[u])
+
+
+@dataclass
+class MinimumInfo:  # landscape.hpp:60-65
+    rank: int
+    fitness: float
+    fraction_of_optimum: float
+    pagerank: float
+
+
+@dataclass
+class CentralityReport:  # landscape.hpp:67-75 (minima as columns, not row objects)
+    kind: int
+    damping: float
+    f_opt: float
+    minima_ranks: np.ndarray
+    minima_fitness: np.ndarray
+    minima_fraction: np.ndarray
+    minima_pagerank: np.ndarray
+    c_p_curve: list
+    pagerank_iterations: int
+    pagerank_sum: float
+    n_edges: int = 0
+    timings_ms: dict = field(default_factory=dict)
+
+    @property
+    def minima(self) -> list[MinimumInfo]:
+        return [MinimumInfo(int(r), float(f), float(q), float(p)) for r, f, q, p in
+                zip(self.minima_ranks, self.minima_fitness, self.minima_fraction,
+                    self.minima_pagerank)]
+
+
+@dataclass
+class MinimaFractionReport:  # landscape.hpp:88-92
+    fractions: np.ndarray
+    median: float = 0.0
+    mean: float = 0.0
+
+
+# -------------------------------------------------------- device handle --
+
+class Landscape:
+    """One search space resident on one GPU (a tk_land handle)."""
+
+    def __init__(self, radix, device: int = 0):
+        self.L = _abi.load()
+        r = np.ascontiguousarray(radix, np.uint32)
+        self.radix = [int(x) for x in r]
+        h = C.c_void_p()
+        _check(self.L.tk_land_create(device, len(r), _ptr(r), C.byref(h)))
+        self.h = h
+        n = C.c_uint64()
+        _check(self.L.tk_land_info(self.h, C.byref(n), None))
+        self.n = n.value
+        self.n_edges = 0
+        self.n_minima = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tk_land_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.L.tk_land_stream(self.h) or 0)
+
+    # ---- ingestion
+    def load_dense(self, fitness, ok, device_ptrs: bool = False):
+        if device_ptrs:  # (fitness_ptr, ok_ptr) as ints
+            _check(self.L.tk_land_load_dense(self.h, C.c_void_p(fitness), C.c_void_p(ok),
+                                             _abi.TK_MEM_DEVICE))
+            return
+        f = np.ascontiguousarray(fitness, np.float64)
+        o = np.ascontiguousarray(ok, np.uint8)
+        if f.shape != (self.n,) or o.shape != (self.n,):
+            raise InvalidArgument("fitness/ok must have one entry per configuration")
+        _check(self.L.tk_land_load_dense(self.h, _ptr(f), _ptr(o), _abi.TK_MEM_HOST))
+
+    def load_sparse(self, keys, fitness):
+        k = np.ascontiguousarray(keys, np.uint64)
+        f = np.ascontiguousarray(fitness, np.float64)
+        _check(self.L.tk_land_load_sparse(self.h, _ptr(k), _ptr(f), k.shape[0],
+                                          _abi.TK_MEM_HOST))
+
+    def load_configs(self, configs, fitness):
+        c = np.ascontiguousarray(configs, np.int32)
+        f = np.ascontiguousarray(fitness, np.float64)
+        if c.ndim != 2 or c.shape[1] != len(self.radix):
+            raise InvalidArgument("configs must be int32[n_valid][dims]")
+        _check(self.L.tk_land_load_configs(self.h, _ptr(c), _ptr(f), c.shape[0],
+                                           _abi.TK_MEM_HOST))
+
+    def generate(self, gen: int, fail_fraction: float, seed: int):
+        _check(self.L.tk_land_generate(self.h, gen, fail_fraction, seed))
+
+    def fitness(self):
+        f = np.empty(self.n, np.float64)
+        o = np.empty(self.n, np.uint8)
+        _check(self.L.tk_land_copy_fitness(self.h, _ptr(f), _ptr(o)))
+        return f, o
+
+    def lookup(self, keys):
+        k = np.ascontiguousarray(keys, np.uint64)
+        f = np.empty(k.shape[0], np.float64)
+        hit = np.empty(k.shape[0], np.uint8)
+        _check(self.L.tk_land_lookup(self.h, _ptr(k), k.shape[0], _ptr(f), _ptr(hit)))
+        return f, hit
+
+    def optimum(self):
+        f, r = C.c_double(), C.c_uint64()
+        _check(self.L.tk_optimum(self.h, C.byref(f), C.byref(r)))
+        return f.value, r.value
+
+    # ---- FFG
+    def build_ffg(self, kind: int, node_limit: int = 1_000_000, emit_csr: bool = True):
+        e, m = C.c_uint64(), C.c_uint64()
+        _check(self.L.tk_ffg_build(self.h, kind, node_limit, int(emit_csr), C.byref(e),
+                                   C.byref(m)))
+        self.kind = kind
+        self.n_edges, self.n_minima = e.value, m.value
+        return self.n_edges, self.n_minima
+
+    def ffg_arrays(self):
+        off = np.empty(self.n + 1, np.uint64)
+        tg = np.empty(max(1, self.n_edges), np.uint32)
+        sk = np.empty(self.n, np.uint8)
+        mn = np.empty(max(1, self.n_minima), np.uint32)
+        _check(self.L.tk_ffg_copy_out(self.h, _ptr(off), _ptr(tg), _ptr(sk), _ptr(mn)))
+        return off, tg[: self.n_edges], sk, mn[: self.n_minima]
+
+    def census(self, with_ranks: bool = True) -> PointCensus:
+        fp, lm, it = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(self.L.tk_census(self.h, C.byref(fp), C.byref(lm), C.byref(it), None))
+        ranks = np.zeros(lm.value, np.uint64)
+        if with_ranks and lm.value:
+            _check(self.L.tk_census(self.h, C.byref(fp), C.byref(lm), C.byref(it), _ptr(ranks)))
+        return PointCensus(self.kind, self.n, fp.value, lm.value, it.value, ranks)
+
+    # ---- PageRank / C_p
+    def pagerank(self, damping=0.85, tol=1e-10, max_iter=100000):
+        it, res, s = C.c_int64(), C.c_double(), C.c_double()
+        st = self.L.tk_pagerank(self.h, damping, tol, max_iter, C.byref(it), C.byref(res),
+                                C.byref(s))
+        _check(st, it.value, res.value)
+        self.iterations, self.residual, self.pagerank_sum = it.value, res.value, s.value
+        return it.value, res.value, s.value
+
+    def pagerank_vector(self):
+        r = np.empty(self.n, np.float64)
+        _check(self.L.tk_pagerank_copy_out(self.h, _ptr(r)))
+        return r
+
+    def centrality(self, f_opt: float, ps):
+        p = np.ascontiguousarray(ps, np.float64)
+        out = np.empty(p.shape[0], np.float64)
+        _check(self.L.tk_centrality(self.h, f_opt, _ptr(p), p.shape[0], _ptr(out)))
+        return out
+
+    def report_rows(self, f_opt: float):
+        m = self.n_minima
+        ranks = np.empty(m, np.uint64)
+        fit = np.empty(m, np.float64)
+        frac = np.empty(m, np.float64)
+        pr = np.empty(m, np.float64)
+        _check(self.L.tk_report_copy_out(self.h, f_opt, _ptr(ranks), _ptr(fit), _ptr(frac),
+                                         _ptr(pr)))
+        return ranks, fit, frac, pr
+
+    def analyze(self, kind: int, damping=0.85, tol=1e-10, max_iter=100000,
+                node_limit=1_000_000, p_max_percent=15, emit_csr=False):
+        s = _abi.ReportSummary()
+        st = self.L.tk_analyze(self.h, kind, damping, tol, max_iter, node_limit,
+                               p_max_percent, int(emit_csr), C.byref(s))
+        _check(st, s.iterations, s.residual)
+        self.kind = kind
+        self.n_edges, self.n_minima = s.n_edges, s.n_minima
+        return s
+
+
+# ------------------------------------------------- reference-shaped calls --
+
+def classify_points(cache: SearchSpaceCache, kind: int) -> PointCensus:
+    """landscape.hpp:24 -- strict census."""
+    with Landscape(cache.radix) as land:
+        land.load_dense(cache.mean_, cache.ok_)
+        land.build_ffg(kind, node_limit=1 << 32, emit_csr=False)
+        return land.census()
+
+
+def build_ffg(cache: SearchSpaceCache, kind: int, node_limit: int = 1_000_000
+              ) -> FitnessFlowGraph:
+    """landscape.hpp:44-45"""
+    with Landscape(cache.radix) as land:
+        land.load_dense(cache.mean_, cache.ok_)
+        land.build_ffg(kind, node_limit, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+        return FitnessFlowGraph(kind, land.n, off, tg, cache.mean_.copy(), sk, mn)
+
+
+def pagerank(g: FitnessFlowGraph, damping: float = 0.85, tol: float = 1e-10,
+             max_iter: int = 100000, device: int = 0) -> np.ndarray:
+    """landscape.hpp:51-52 -- arbitrary out-CSR, transposed and iterated on the GPU."""
+    L = _abi.load()
+    off = np.ascontiguousarray(g.offsets, np.uint64)
+    tg = np.ascontiguousarray(g.targets, np.uint32)
+    n = off.shape[0] - 1
+    r = np.empty(max(1, n), np.float64)
+    it, res = C.c_int64(), C.c_double()
+    st = L.tk_pagerank_csr(device, n, _ptr(off), _ptr(tg) if tg.size else None, damping, tol,
+                           max_iter, _ptr(r), C.byref(it), C.byref(res))
+    _check(st, it.value, res.value)
+    pagerank.last_iterations = it.value
+    return r[:n]
+
+
+def proportion_of_centrality(g: FitnessFlowGraph, pr, f_opt: float, p: float,
+                             device: int = 0) -> float:
+    """landscape.hpp:56-58 (SURVEY.md A8 threshold)."""
+    L = _abi.load()
+    mins = np.ascontiguousarray(g.minima, np.int64)
+    mf = np.ascontiguousarray(np.asarray(g.fitness)[mins], np.float64)
+    mp = np.ascontiguousarray(np.asarray(pr)[mins], np.float64)
+    out = C.c_double()
+    _check(L.tk_proportion_of_centrality(device, mins.shape[0], _ptr(mf), _ptr(mp), f_opt, p,
+                                         C.byref(out)))
+    return out.value
+
+
+def analyze_landscape(cache: SearchSpaceCache, kind: int, damping: float = 0.85,
+                      p_max_percent: int = 15, node_limit: int = 1_000_000,
+                      tol: float = 1e-10, max_iter: int = 100000) -> CentralityReport:
+    """landscape.hpp:77-79, plus the node_limit overload."""
+    with Landscape(cache.radix) as land:
+        land.load_dense(cache.mean_, cache.ok_)
+        s = land.analyze(kind, damping, tol, max_iter, node_limit, p_max_percent)
+        ranks, fit, frac, prv = land.report_rows(s.f_opt)
+        return CentralityReport(kind, damping, s.f_opt, ranks, fit, frac, prv,
+                                [(k, s.c_p[k]) for k in range(s.n_cp)], s.iterations,
+                                s.pagerank_sum, s.n_edges,
+                                dict(ffg=s.ms_ffg, pagerank=s.ms_pagerank,
+                                     centrality=s.ms_centrality))
+
+
+def minima_fraction_report(cache: SearchSpaceCache, kind: int) -> MinimaFractionReport:
+    """landscape.hpp:87-94: f_opt / f over the FFG minima, ascending."""
+    with Landscape(cache.radix) as land:
+        land.load_dense(cache.mean_, cache.ok_)
+        land.build_ffg(kind, node_limit=1 << 32, emit_csr=False)
+        f_opt, _ = land.optimum()
+        land.pagerank()  # report rows need a rank vector; cheap next to the FFG
+        _, _, frac, _ = land.report_rows(f_opt)
+    fr = np.sort(frac)
+    if fr.size == 0:
+        return MinimaFractionReport(fr)
+    return MinimaFractionReport(fr, float(np.median(fr)), float(fr.mean()))

@@ -1,0 +1,44 @@
+#!/usr/bin/env bash
+# One gpurun session: parity tests, smoke, bench, ncu launch list and captures.
+#   gpurun --timeout 2400 -- 'bash scripts/gpu_session.sh [tag] [what]'
+# what: all (default) | tests | bench | ncu
+set -u
+TAG=${1:-r01}
+WHAT=${2:-all}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+export PYTHONUNBUFFERED=1
+nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
+nproc > "$OUT/host.txt"; lscpu | grep -E 'Model name|^CPU\(s\)' >> "$OUT/host.txt"
+
+if [[ $WHAT == all || $WHAT == tests ]]; then
+  timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > "$OUT/pytest_gpu.log" 2>&1
+  echo "exit=$?" >> "$OUT/pytest_gpu.log"
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
+  echo "exit=$?" >> "$OUT/smoke.log"
+fi
+
+if [[ $WHAT == all || $WHAT == bench ]]; then
+  timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+  echo "exit=$?" >> "$OUT/bench.err"
+  timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
+fi
+
+if [[ $WHAT == all || $WHAT == ncu ]]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu \
+      > "$OUT/ncu_launches.log" 2>&1
+  echo "exit=$?" >> "$OUT/ncu_launches.log"
+  timeout 900 ncu --set full --clock-control none --import-source on \
+      -k regex:ffg_build_kernel -s 3 -c 1 -o "$OUT/prof_ffg" \
+      python bench.py --steps 1 --warmup 3 --no-cpu > "$OUT/ncu_ffg.log" 2>&1
+  echo "exit=$?" >> "$OUT/ncu_ffg.log"
+  timeout 1200 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis \
+      --section LaunchStats --section Occupancy --section WarpStateStats --section SourceCounters \
+      --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
+      --clock-control none --import-source on \
+      -k regex:pagerank_kernel -s 3 -c 1 -o "$OUT/prof_pr" \
+      python bench.py --steps 1 --warmup 3 --no-cpu > "$OUT/ncu_pr.log" 2>&1
+  echo "exit=$?" >> "$OUT/ncu_pr.log"
+fi
+ls -la "$OUT"

@@ -1,0 +1,286 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle and the
+golden fixtures of the reference's own code.
+
+Bars (BASELINE.json north_star): FFG CSR, is_sink and minima bit-exact;
+PageRank within 1e-12 relative L1 with the same iteration count; C_p within
+1e-9 absolute.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+PR_RTOL = 1e-12  # relative L1 on the rank vector
+CP_ATOL = 1e-9   # absolute on C_p
+
+
+@pytest.fixture(scope="module")
+def tk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2210_01465_b200 as tk
+
+    tk._abi.load()
+    return tk
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rel_l1(a, b):
+    return float(np.abs(a - b).sum() / np.abs(b).sum())
+
+
+def gpu_ffg(tk, radix, fit, ok, kind):
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(kind, node_limit=1 << 32, emit_csr=True)
+        return land.ffg_arrays()
+
+
+# ------------------------------------------------------------------ inputs --
+
+@pytest.mark.parametrize("gen", [0, 1])
+def test_device_generators_bit_identical(tk, gen):
+    n = 1 << 20
+    with tk.Landscape([1 << 10, 1 << 10]) as land:
+        land.generate(gen, 0.3, 17)
+        f, o = land.fitness()
+    rf, ro = (O.gen_iid if gen == 0 else O.gen_heavy)(n, 0.3, 17, nthreads=8)
+    assert np.array_equal(f.view(np.uint64), rf.view(np.uint64))
+    assert np.array_equal(o, ro)
+
+
+def test_sparse_hash_ingest_matches_dense(tk):
+    radix = [12, 6, 8, 8, 2, 2]
+    fit, ok = O.gen_synthetic(radix, 0.68, "rugged", 3)
+    keys = np.flatnonzero(ok).astype(np.uint64)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(keys.shape[0])
+    with tk.Landscape(radix) as land:
+        land.load_sparse(keys[perm], fit[keys][perm])
+        f, o = land.fitness()
+        assert np.array_equal(f.view(np.uint64), fit.view(np.uint64))
+        assert np.array_equal(o, ok)
+        q = np.array([keys[0], keys[-1], 0, len(fit) - 1], np.uint64)
+        lf, hit = land.lookup(q)
+        assert list(hit) == [1, 1, ok[0], ok[-1]]
+        assert lf[0] == fit[keys[0]]
+        # configurations as index vectors -> mixed-radix keys on the device
+        strides = O.strides(radix).astype(np.int64)
+        cfg = np.stack([(keys.astype(np.int64) // s) % m for s, m in zip(strides, radix)], 1)
+        land.load_configs(cfg.astype(np.int32), fit[keys])
+        f2, o2 = land.fitness()
+        assert np.array_equal(f2.view(np.uint64), fit.view(np.uint64))
+        assert np.array_equal(o2, ok)
+        with pytest.raises(tk.InvalidArgument):
+            land.load_sparse(np.array([1, 2, 1], np.uint64), np.ones(3))
+        with pytest.raises(tk.InvalidArgument):
+            land.load_sparse(np.array([len(fit)], np.uint64), np.ones(1))
+        bad = cfg[:2].copy()
+        bad[1, 0] = radix[0]
+        with pytest.raises(tk.InvalidArgument):
+            land.load_configs(bad.astype(np.int32), np.ones(2))
+
+
+# --------------------------------------------------------------------- FFG --
+
+@pytest.mark.parametrize("kind", [O.HAMMING, O.ADJACENT])
+def test_ffg_matches_reference_golden(tk, golden, kind):
+    meta, arrays = golden
+    for rec in meta["synthetic"]:
+        fit, ok = O.gen_synthetic(rec["radix"], rec["q"], rec["profile"], rec["seed"])
+        off, tg, sk, mn = gpu_ffg(tk, rec["radix"], fit, ok, kind)
+        ref = rec["ffg"][str(kind)]
+        assert len(tg) == ref["edges"], rec["key"]
+        assert sha(off) == ref["sha_offsets"], rec["key"]
+        assert sha(tg) == ref["sha_targets"], rec["key"]
+        assert sha(sk) == ref["sha_is_sink"], rec["key"]
+        assert sha(mn) == ref["sha_minima"], rec["key"]
+
+
+@pytest.mark.parametrize("radix,kind,gen", [
+    ([12, 12, 12, 12], O.ADJACENT, "iid"),               # C1, packed masks
+    ([16, 12, 8, 8, 8, 4, 2, 2], O.ADJACENT, "syn"),     # C2 shape
+    ([2] * 16, O.ADJACENT, "iid"),                       # 32 ordered slots (u32, unpacked)
+    ([2] * 20, O.ADJACENT, "iid"),                       # 40 ordered slots (u64)
+    ([3] * 14, O.HAMMING, "heavy"),                      # 28 Hamming slots
+    ([8, 8, 6, 6, 4, 4, 2], O.HAMMING, "iid"),           # 33 Hamming slots (u64)
+    ([5, 1, 7, 1, 3], O.ADJACENT, "syn"),                # singleton dims are dropped
+    ([1], O.ADJACENT, "iid"),                            # single node
+])
+def test_ffg_and_census_bit_exact(tk, radix, kind, gen):
+    n = O.space_size(radix)
+    if gen == "iid":
+        fit, ok = O.gen_iid(n, 0.2, 5)
+    elif gen == "heavy":
+        fit, ok = O.gen_heavy(n, 0.1, 6)
+    else:
+        fit, ok = O.gen_synthetic(radix, 0.3, "rugged", 7)
+    ref = O.build_ffg(radix, fit, ok, kind, node_limit=1 << 32, nthreads=8)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(kind, node_limit=1 << 32, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+        cen = land.census()
+    assert np.array_equal(off, ref["offsets"])
+    assert np.array_equal(tg, ref["targets"])
+    assert np.array_equal(sk, ref["is_sink"])
+    assert np.array_equal(mn, ref["minima"])
+    rc = O.census(radix, fit, ok, kind)
+    assert cen.fail_points == rc["fail_points"]
+    assert cen.local_minima == rc["local_minima"]
+    assert cen.interior == rc["interior"]
+    assert np.array_equal(cen.minima_ranks, rc["minima_ranks"])
+
+
+def test_census_with_ties(tk):
+    # SPEC.md:387 constant space: no strict minima, every ok node an FFG minimum
+    radix = [4, 3, 5]
+    fit = np.full(60, 2.5)
+    ok = np.ones(60, np.uint8)
+    ok[7] = 0
+    fit[7] = 1e10
+    for kind in (O.HAMMING, O.ADJACENT):
+        with tk.Landscape(radix) as land:
+            land.load_dense(fit, ok)
+            _, m = land.build_ffg(kind)
+            c = land.census()
+        assert c.local_minima == 0 and c.fail_points == 1 and c.interior == 59
+        assert m == 59
+
+
+def test_node_limit_and_errors(tk):
+    with tk.Landscape([64, 64]) as land:
+        fit, ok = O.gen_iid(4096, 0.0, 1)
+        land.load_dense(fit, ok)
+        with pytest.raises(tk.InvalidArgument, match="node limit"):
+            land.build_ffg(O.ADJACENT, node_limit=4095)
+        with pytest.raises(tk.Error):
+            land.pagerank()  # build first
+    with tk.Landscape([3, 3]) as land:
+        land.load_dense(np.full(9, 1e10), np.zeros(9, np.uint8))
+        with pytest.raises(tk.NoFeasiblePoint):
+            land.analyze(O.ADJACENT)
+
+
+# ---------------------------------------------------------------- PageRank --
+
+@pytest.mark.parametrize("radix,kind", [
+    ([12, 12, 12, 12], O.ADJACENT),
+    ([2] * 16, O.ADJACENT),
+    ([2] * 20, O.ADJACENT),
+    ([3] * 10, O.HAMMING),
+    ([8, 8, 6, 6, 4, 4, 2], O.HAMMING),
+    ([16, 12, 8, 8, 8, 4, 2, 2], O.ADJACENT),
+])
+def test_pagerank_structured_matches_oracle(tk, radix, kind):
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, 0.25, 11)
+    ref = O.analyze(radix, fit, ok, kind, nthreads=1, node_limit=1 << 32)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(kind, node_limit=1 << 32, emit_csr=False)
+        it, res, s = land.pagerank()
+        r = land.pagerank_vector()
+        f_opt, orank = land.optimum()
+        cps = land.centrality(f_opt, [k / 100.0 for k in range(16)])
+    assert it == ref["iterations"]
+    assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
+    assert abs(s - 1.0) < 1e-9
+    assert (f_opt, orank) == (ref["f_opt"], ref["opt_rank"])
+    assert np.max(np.abs(cps - [c for _, c in ref["c_p_curve"]])) <= CP_ATOL
+
+
+def test_pagerank_csr_dropin_matches_oracle(tk):
+    radix = [8, 6, 3, 3, 2]
+    fit, ok = O.gen_synthetic(radix, 0.52, "rugged", 2)
+    cache = tk.SearchSpaceCache(radix, fit, ok)
+    for kind in (O.HAMMING, O.ADJACENT):
+        g = tk.build_ffg(cache, kind)
+        r = tk.pagerank(g)
+        ref, it, _ = O.pagerank(g.offsets, g.targets)
+        assert tk.pagerank.last_iterations == it
+        assert rel_l1(r, ref) <= PR_RTOL
+        f_opt = cache.optimum()
+        for p in (0.0, 0.01, 0.05, 0.15, 3.0):
+            got = tk.proportion_of_centrality(g, r, f_opt, p)
+            exp = O.proportion_of_centrality(g.minima, fit, ref, f_opt, p)
+            assert abs(got - exp) <= CP_ATOL
+
+
+def test_pagerank_spec_examples(tk):
+    FFG = tk.FitnessFlowGraph
+    one = FFG(O.ADJACENT, 1, np.array([0, 0], np.uint64), np.zeros(0, np.uint32),
+              np.ones(1), np.ones(1, np.uint8), np.zeros(1, np.uint32))
+    assert tk.pagerank(one)[0] == 1.0
+    ab = FFG(O.ADJACENT, 2, np.array([0, 1, 1], np.uint64), np.array([1], np.uint32),
+             np.array([2.0, 1.0]), np.array([0, 1], np.uint8), np.array([1], np.uint32))
+    r = tk.pagerank(ab, damping=1.0, tol=1e-15)
+    assert abs(r[0] - 1 / 3) < 1e-14 and abs(r[1] - 2 / 3) < 1e-14
+    with pytest.raises(tk.NonConvergence) as e:
+        tk.pagerank(ab, max_iter=3)
+    assert e.value.iterations == 3 and e.value.residual > 0
+    for bad in (dict(damping=1.5), dict(tol=0.0), dict(max_iter=0)):
+        with pytest.raises(tk.InvalidArgument):
+            tk.pagerank(ab, **bad)
+
+
+def test_analyze_landscape_matches_oracle(tk, golden):
+    meta, _ = golden
+    for rec in meta["synthetic"]:
+        if rec["status"] != 0:
+            continue
+        fit, ok = O.gen_synthetic(rec["radix"], rec["q"], rec["profile"], rec["seed"])
+        cache = tk.SearchSpaceCache(rec["radix"], fit, ok)
+        for kind in (O.HAMMING, O.ADJACENT):
+            rep = tk.analyze_landscape(cache, kind)
+            ref = O.analyze(rec["radix"], fit, ok, kind)
+            assert rep.f_opt == rec["f_opt"]
+            assert rep.pagerank_iterations == ref["iterations"]
+            mins = ref["ffg"]["minima"]
+            assert np.array_equal(rep.minima_ranks, mins.astype(np.uint64))
+            assert np.array_equal(rep.minima_fitness, fit[mins])
+            assert np.array_equal(rep.minima_fraction, rec["f_opt"] / fit[mins])
+            assert rel_l1(rep.minima_pagerank, ref["pagerank"][mins]) <= 1e-11
+            assert abs(rep.pagerank_sum - 1.0) < 1e-9
+            for (k, c), (k2, c2) in zip(rep.c_p_curve, ref["c_p_curve"]):
+                assert k == k2 and abs(c - c2) <= CP_ATOL
+
+
+# ------------------------------------------- full-size, size-independent checks --
+
+@pytest.mark.parametrize("radix,kind,gen,q", [
+    ([8, 8, 8, 8, 6, 6, 4, 4, 2, 2], O.ADJACENT, 1, 0.0),   # C3 shape, heavy tails
+    ([8, 8, 8, 8, 6, 6, 4, 4, 2, 2], O.HAMMING, 1, 0.0),
+])
+def test_c3_scale_properties_and_parity(tk, radix, kind, gen, q):
+    n = O.space_size(radix)
+    with tk.Landscape(radix) as land:
+        land.generate(gen, q, 3)
+        e, m = land.build_ffg(kind, node_limit=1 << 32, emit_csr=True)
+        # tie-free, no failures: E is structural
+        if kind == O.ADJACENT:
+            assert e == sum(n * (mm - 1) // mm for mm in radix)
+        else:
+            assert e == sum(n * (mm - 1) // 2 for mm in radix)
+        off, tg, sk, mn = land.ffg_arrays()
+        fit, ok = land.fitness()
+        it, res, s = land.pagerank()
+        r = land.pagerank_vector()
+        f_opt, _ = land.optimum()
+        cps = land.centrality(f_opt, [k / 100.0 for k in range(16)])
+    ref = O.build_ffg(radix, fit, ok, kind, node_limit=1 << 32, nthreads=8)
+    assert np.array_equal(off, ref["offsets"]) and np.array_equal(tg, ref["targets"])
+    assert np.array_equal(mn, ref["minima"])
+    assert abs(s - 1.0) < 1e-9 and res < 1e-10
+    assert np.all(np.diff(cps) >= -1e-15) and 0 <= cps[0] and cps[-1] <= 1 + 1e-15
+    rr, rit, _ = O.pagerank(off, tg, nthreads=8)
+    assert it == rit and rel_l1(r, rr) <= PR_RTOL
