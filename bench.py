@@ -272,12 +272,13 @@ def run_b200(args, wl, kind):
     pr_bytes = per_pro + per_iter * it_last
     achieved = pr_bytes / (pr_ms / 1e3) / 1e9
     ffg_ms = float(np.mean([x.ms_ffg for x in sums]))
+    kinfo = land.kernel_info()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                 "traffic": None, "kernel": "pagerank_kernel (persistent, cooperative)",
                 "bytes_model": model, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pr_bytes, "kernel_ms": round(pr_ms, 3),
-                "iterations": it_last}
+                "iterations": it_last, "kernels": kinfo}
 
     out = None
     if rank == 0:

@@ -84,6 +84,11 @@ int tk_land_destroy(tk_land* land);
 int tk_land_info(const tk_land* land, uint64_t* n_nodes, int* device);
 /* The cudaStream_t every kernel of this handle is launched on (for events). */
 void* tk_land_stream(tk_land* land);
+/* Which kernels the last build / PageRank used (1 = TMA-staged Adjacent path,
+ * 0 = per-lane gathers), the PageRank grid size and the kernel-only device
+ * times of the last build and PageRank launches (ms).  Any pointer may be NULL. */
+int tk_land_kernel_info(const tk_land* land, int* staged_build, int* staged_pagerank,
+                        int* pagerank_grid, float* ms_build, float* ms_pagerank);
 
 /* SearchSpaceCache::mean/ok (cache.hpp:42-48): rank-indexed fitness (failed
  * entries carry kFailFitness = 1e10, cache.hpp:15) and ok flags.  The cache

@@ -1,0 +1,18 @@
+// tunekit_b200/extensions.hpp -- additions beyond the reference's landscape.hpp.
+#pragma once
+
+#include <cstdint>
+
+#include "tunekit/landscape.hpp"
+
+namespace tunekit {
+
+// analyze_landscape with an explicit FFG node limit.  The reference's
+// analyze_landscape (landscape.hpp:77-79) has no node_limit parameter while
+// build_ffg defaults to 1e6 (landscape.hpp:44-45), so spaces above 1e6
+// configurations need this overload.
+CentralityReport analyze_landscape_limited(const SearchSpaceCache& cache, NeighbourhoodKind kind,
+                                           double damping, int p_max_percent,
+                                           std::uint64_t node_limit);
+
+}  // namespace tunekit

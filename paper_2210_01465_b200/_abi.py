@@ -22,6 +22,7 @@ TK_MAX_CP = 101
 EXPORTS = [
     "tk_abi_version", "tk_last_error", "tk_status_name", "tk_device_count",
     "tk_land_create", "tk_land_destroy", "tk_land_info", "tk_land_stream",
+    "tk_land_kernel_info",
     "tk_land_load_dense", "tk_land_load_sparse", "tk_land_load_configs",
     "tk_land_generate", "tk_land_copy_fitness", "tk_land_lookup", "tk_optimum",
     "tk_ffg_build", "tk_ffg_copy_out", "tk_census", "tk_pagerank",
@@ -64,6 +65,8 @@ def load(path: str = LIB_PATH):
         "tk_land_destroy": (I, [P]),
         "tk_land_info": (I, [P, PU64, C.POINTER(I)]),
         "tk_land_stream": (P, [P]),
+        "tk_land_kernel_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I),
+                                    C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "tk_land_load_dense": (I, [P, P, P, I]),
         "tk_land_load_sparse": (I, [P, P, P, U64, I]),
         "tk_land_load_configs": (I, [P, P, P, U64, I]),

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -58,6 +59,16 @@ cudaError_t ensure(DevBuf& b, size_t bytes) {
 }
 
 constexpr uint64_t kMaxNodes = 0xFFF00000ull;  // u32 ids with grid-stride headroom
+// per-rank arrays are padded so tile-granular bulk copies may round the last
+// tile up to 16 elements (tk_staged.cu)
+constexpr uint64_t kPad = 16;
+
+// TK_KERNELS=v1 selects the per-lane-gather kernels instead of the TMA-staged
+// ones (A/B comparisons and parity tests of both paths).
+bool staged_enabled() {
+    const char* e = std::getenv("TK_KERNELS");
+    return !(e && std::string(e) == "v1");
+}
 
 struct PrOut {
     long long iter;
@@ -83,6 +94,7 @@ struct Small {  // device-side scalars read back by the host
 struct tk_land {
     int device = 0;
     int num_sms = 148;
+    int smem_optin = 0;  // max dynamic shared memory per block
     cudaStream_t stream = nullptr;
     std::vector<uint32_t> radix_in;
     std::vector<unsigned long long> strides_in;
@@ -110,6 +122,8 @@ struct tk_land {
     Small* hsmall = nullptr;  // pinned mirror
     cudaEvent_t ev[6] = {};
     float ms_build = 0.f, ms_pr = 0.f;  // kernel-only device time of the last launch
+    bool staged = false;                // last build used the TMA-staged kernel
+    bool pr_staged = false;             // last PageRank used the TMA-staged kernel
     int pr_grid = 0;
 };
 
@@ -187,7 +201,7 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     const uint32_t ntiles = static_cast<uint32_t>((n + tk::kBuildThreads - 1) / tk::kBuildThreads);
     TKC(set_dev(l));
     if (mode == tk::MODE_ADJ_PACKED) {
-        TKC(ensure(l->pw, n * 4));
+        TKC(ensure(l->pw, (n + kPad) * 4));
     } else {
         TKC(ensure(l->inm, n * (wide ? 8 : 4)));
         TKC(ensure(l->odeg, n));
@@ -223,7 +237,15 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     a.totals = ds->totals;
     a.ntiles = ntiles;
     TKC(cudaEventRecord(l->ev[0], l->stream));
-    TKC(tk::launch_ffg_build(s, mode, wide, emit != 0, a, l->num_sms, l->stream));
+    tk::StagePlan plan{};
+    if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+        tk::make_stage_plan(s, false, l->smem_optin - 4096, &plan)) {
+        TKC(tk::launch_ffg_build_staged(s, plan, emit != 0, a, l->num_sms, l->stream));
+        l->staged = true;
+    } else {
+        TKC(tk::launch_ffg_build(s, mode, wide, emit != 0, a, l->num_sms, l->stream));
+        l->staged = false;
+    }
     TKC(cudaEventRecord(l->ev[1], l->stream));
     TKC(cudaMemcpyAsync(l->hsmall->totals, ds->totals, sizeof(ds->totals),
                         cudaMemcpyDeviceToHost, l->stream));
@@ -279,9 +301,10 @@ int nonconv(long long it, double res) {
 int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool wide,
                  tk::PrArgs a, DevBuf& part, Small* ds, Small* hs, cudaStream_t stream,
                  double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
-                 cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr) {
+                 cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr,
+                 const tk::StagePlan* plan = nullptr) {
     (void)device;
-    const int maxg = tk::pagerank_max_grid(mode, wide, num_sms);
+    const int maxg = plan ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
     TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
     const double nd = static_cast<double>(a.n);
@@ -299,7 +322,8 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
     a.out_status = &ds->pr.status;
     int g = 0;
     if (e0) TKC(cudaEventRecord(e0, stream));
-    TKC(tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream));
+    if (plan) TKC(tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream));
+    else TKC(tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream));
     if (e1) TKC(cudaEventRecord(e1, stream));
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
     TKC(cudaStreamSynchronize(stream));
@@ -314,10 +338,10 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     if (st) return st;
     TKC(set_dev(l));
     const uint64_t n = l->n;
-    TKC(ensure(l->r0, n * 8));
-    TKC(ensure(l->r1, n * 8));
-    TKC(ensure(l->c0, n * 8));
-    TKC(ensure(l->c1, n * 8));
+    TKC(ensure(l->r0, (n + kPad) * 8));
+    TKC(ensure(l->r1, (n + kPad) * 8));
+    TKC(ensure(l->c0, (n + kPad) * 8));
+    TKC(ensure(l->c1, (n + kPad) * 8));
     tk::PrArgs a{};
     a.n = static_cast<uint32_t>(n);
     a.pw = l->pw.as<uint32_t>();
@@ -327,10 +351,14 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     a.r1 = l->r1.as<double>();
     a.c0 = l->c0.as<double>();
     a.c1 = l->c1.as<double>();
+    tk::StagePlan plan{};
+    const bool have_plan = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+                           tk::make_stage_plan(l->shape, true, l->smem_optin - 4096, &plan);
+    l->pr_staged = have_plan;
     l->pr_done = false;
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
                       l->small.as<Small>(), l->hsmall, l->stream, d, tol, max_iter, l->ev[2],
-                      l->ev[3], &l->ms_pr, &l->pr_grid);
+                      l->ev[3], &l->ms_pr, &l->pr_grid, have_plan ? &plan : nullptr);
     if (st) return st;
     const PrOut& o = l->hsmall->pr;
     l->iterations = o.iter;
@@ -377,8 +405,8 @@ int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const doubl
     while (cap < 2 * nv) cap <<= 1;
     TKC(ensure(l->hkeys, cap * 8));
     TKC(ensure(l->hvals, cap * 8));
-    TKC(ensure(l->fit, l->n * 8));
-    TKC(ensure(l->ok, l->n));
+    TKC(ensure(l->fit, (l->n + kPad) * 8));
+    TKC(ensure(l->ok, l->n + kPad));
     l->hcap = cap;
     Small* ds = l->small.as<Small>();
     TKC(cudaMemsetAsync(l->hkeys.p, 0xFF, cap * 8, l->stream));
@@ -472,6 +500,7 @@ int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** o
     cudaError_t e = cudaGetDeviceProperties(&prop, device);
     if (e == cudaSuccess) {
         l->num_sms = prop.multiProcessorCount;
+        l->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
         if (!prop.cooperativeLaunch) e = cudaErrorNotSupported;
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking);
@@ -514,12 +543,23 @@ int tk_land_info(const tk_land* l, uint64_t* n_nodes, int* device) {
 
 void* tk_land_stream(tk_land* l) { return l ? static_cast<void*>(l->stream) : nullptr; }
 
+int tk_land_kernel_info(const tk_land* l, int* staged_build, int* staged_pagerank,
+                        int* pagerank_grid, float* ms_build, float* ms_pagerank) {
+    if (int st = check_land(l)) return st;
+    if (staged_build) *staged_build = l->staged ? 1 : 0;
+    if (staged_pagerank) *staged_pagerank = l->pr_staged ? 1 : 0;
+    if (pagerank_grid) *pagerank_grid = l->pr_grid;
+    if (ms_build) *ms_build = l->ms_build;
+    if (ms_pagerank) *ms_pagerank = l->ms_pr;
+    return TK_OK;
+}
+
 int tk_land_load_dense(tk_land* l, const double* fitness, const uint8_t* ok, int mem) {
     if (int st = check_land(l)) return st;
     if (!fitness || !ok) return fail(TK_EINVAL, "load_dense: null buffer");
     TKC(set_dev(l));
-    TKC(ensure(l->fit, l->n * 8));
-    TKC(ensure(l->ok, l->n));
+    TKC(ensure(l->fit, (l->n + kPad) * 8));
+    TKC(ensure(l->ok, l->n + kPad));
     TKC(cudaMemcpyAsync(l->fit.p, fitness, l->n * 8, h2x(mem), l->stream));
     TKC(cudaMemcpyAsync(l->ok.p, ok, l->n, h2x(mem), l->stream));
     TKC(cudaStreamSynchronize(l->stream));
@@ -589,8 +629,8 @@ int tk_land_generate(tk_land* l, int gen, double fail_fraction, uint64_t seed) {
     if (!(fail_fraction >= 0.0 && fail_fraction < 1.0))
         return fail(TK_EINVAL, "fail_fraction must be in [0, 1)");
     TKC(set_dev(l));
-    TKC(ensure(l->fit, l->n * 8));
-    TKC(ensure(l->ok, l->n));
+    TKC(ensure(l->fit, (l->n + kPad) * 8));
+    TKC(ensure(l->ok, l->n + kPad));
     TKC(tk::launch_generate(gen, static_cast<uint32_t>(l->n), fail_fraction, seed,
                             l->fit.as<double>(), l->ok.as<uint8_t>(), l->stream));
     TKC(cudaStreamSynchronize(l->stream));

@@ -103,6 +103,35 @@ cudaError_t launch_pagerank(const DevShape& s, int mode, bool wide, const PrArgs
                             int num_sms, int* grid_out, cudaStream_t stream);
 int pagerank_max_grid(int mode, bool wide, int num_sms);
 
+// ---- TMA-staged Adjacent kernels (tk_staged.cu) ------------------------------
+// A tile is T consecutive ranks [v0, v0+T).  The Adjacent neighbours of the tile
+// along dimension i are the contiguous ranges [v0 - s_i, v0 - s_i + T) and
+// [v0 + s_i, v0 + s_i + T), so the block stages, per tile, one "near window"
+// [v0 - H, v0 + T + H) covering every dimension with s_i <= H plus one range
+// per far slot, each with a single cp.async.bulk into shared memory.
+struct StagePlan {
+    int T;           // ranks per tile (= threads per block)
+    int stages;      // pipeline depth
+    int H;           // near halo (elements)
+    int nfar;        // far ranges
+    long long far_off[2 * kMaxDims];  // element offset of far range f from v0
+    int lo_src[kMaxDims];  // f64 smem index (plus t) of the lower neighbour of dim i
+    int hi_src[kMaxDims];  // ... upper neighbour
+    int own_src;           // ... of the node itself
+    int near_len;          // elements in the near window (even)
+    int far_len;           // elements per far range (even)
+    int aux_bytes;         // bytes before the f64 region (pw + r for PageRank, ok for FFG)
+    int stage_bytes;
+    unsigned long long npad2;  // f64 arrays hold at least this many elements (even)
+    unsigned long long npad16; // u8/u32 arrays are padded to this many elements
+};
+// kind_pr: PageRank layout (u32 pw[T], f64 r[T], window) vs FFG (u8 ok[T], window)
+bool make_stage_plan(const DevShape& s, bool kind_pr, int smem_budget, StagePlan* plan);
+cudaError_t launch_ffg_build_staged(const DevShape& s, const StagePlan& p, bool emit,
+                                    const BuildArgs& a, int num_sms, cudaStream_t stream);
+cudaError_t launch_pagerank_staged(const DevShape& s, const StagePlan& p, const PrArgs& a,
+                                   int num_sms, int* grid_out, cudaStream_t stream);
+
 // ---- C_p and report -------------------------------------------------------
 constexpr int kCpBlocks = 148;
 // minima == nullptr: fit/r are already per-minimum arrays of length m.

@@ -217,6 +217,14 @@ class Landscape:
     def stream(self) -> int:
         return int(self.L.tk_land_stream(self.h) or 0)
 
+    def kernel_info(self) -> dict:
+        sb, sp, g = C.c_int(), C.c_int(), C.c_int()
+        mb, mp = C.c_float(), C.c_float()
+        _check(self.L.tk_land_kernel_info(self.h, C.byref(sb), C.byref(sp), C.byref(g),
+                                          C.byref(mb), C.byref(mp)))
+        return dict(staged_build=bool(sb.value), staged_pagerank=bool(sp.value),
+                    pagerank_grid=g.value, ms_build=mb.value, ms_pagerank=mp.value)
+
     # ---- ingestion
     def load_dense(self, fitness, ok, device_ptrs: bool = False):
         if device_ptrs:  # (fitness_ptr, ok_ptr) as ints

@@ -118,7 +118,9 @@ def main() -> None:
                 arrays[f"{key}_k{kind}_minima"] = mn[:M]
         meta["synthetic"].append(rec)
 
-    for nn, kk, seed in [(10, 3, 5), (16, 4, 1), (12, 0, 2)]:
+    # k = 0 is left out: the reference's link loop (generators.cpp:38-44) never
+    # stops at k = 0 and indexes past its 2-entry tables (undefined behaviour).
+    for nn, kk, seed in [(10, 3, 5), (16, 4, 1), (12, 1, 2)]:
         fit = np.empty(1 << nn, np.float64)
         assert R.ref_generate_nk(nn, kk, seed, fit) == 0
         key = f"nk_{nn}_{kk}_{seed}"

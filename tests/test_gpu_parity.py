@@ -199,6 +199,42 @@ def test_pagerank_structured_matches_oracle(tk, radix, kind):
     assert np.max(np.abs(cps - [c for _, c in ref["c_p_curve"]])) <= CP_ATOL
 
 
+@pytest.mark.parametrize("path", ["staged", "v1"])
+@pytest.mark.parametrize("radix,q", [
+    ([8, 8, 8, 6, 6, 6, 4, 4, 4, 4, 2, 1], 0.1),   # C5 shape minus its last dim
+    ([12, 12, 12, 12], 0.0),
+    ([7, 5, 3, 2, 9], 0.3),                         # odd strides: unaligned ranges
+    ([1000, 3], 0.2),                               # near window only / far only
+    ([3, 1000], 0.2),
+    ([2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2], 0.5),  # 26 slots, packed limit
+    ([5], 0.0),
+])
+def test_staged_and_v1_paths_match_oracle(tk, monkeypatch, path, radix, q):
+    if path == "v1":
+        monkeypatch.setenv("TK_KERNELS", "v1")
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, q, 23)
+    if q == 0.0 and n < 100:
+        ok[:] = 1
+    ref = O.build_ffg(radix, fit, ok, O.ADJACENT, node_limit=1 << 32, nthreads=8)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(O.ADJACENT, node_limit=1 << 32, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+        cen = land.census()
+        it, res, s = land.pagerank()
+        r = land.pagerank_vector()
+        info = land.kernel_info()
+    assert info["staged_build"] == (path == "staged")
+    assert info["staged_pagerank"] == (path == "staged")
+    assert np.array_equal(off, ref["offsets"]) and np.array_equal(tg, ref["targets"])
+    assert np.array_equal(sk, ref["is_sink"]) and np.array_equal(mn, ref["minima"])
+    rc = O.census(radix, fit, ok, O.ADJACENT)
+    assert np.array_equal(cen.minima_ranks, rc["minima_ranks"])
+    rr, rit, _ = O.pagerank(ref["offsets"], ref["targets"], nthreads=1)
+    assert it == rit and rel_l1(r, rr) <= PR_RTOL
+
+
 def test_pagerank_csr_dropin_matches_oracle(tk):
     radix = [8, 6, 3, 3, 2]
     fit, ok = O.gen_synthetic(radix, 0.52, "rugged", 2)
