@@ -240,6 +240,7 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     tk::StagePlan plan{};
     if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
         tk::make_stage_plan(s, false, l->smem_optin - 4096, &plan)) {
+        a.ntiles = static_cast<uint32_t>((n + plan.T - 1) / plan.T);  // staged tiles are T ranks
         TKC(tk::launch_ffg_build_staged(s, plan, emit != 0, a, l->num_sms, l->stream));
         l->staged = true;
     } else {

@@ -11,14 +11,17 @@ export PYTHONUNBUFFERED=1
 nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
 nproc > "$OUT/host.txt"; lscpu | grep -E 'Model name|^CPU\(s\)' >> "$OUT/host.txt"
 
-if [[ $WHAT == all || $WHAT == tests ]]; then
-  timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > "$OUT/pytest_gpu.log" 2>&1
+if [[ $WHAT == all || $WHAT == tests || $WHAT == quick ]]; then
+  timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 \
+      python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/sanitizer_smoke.log" 2>&1
+  echo "exit=$?" >> "$OUT/sanitizer_smoke.log"
+  timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > "$OUT/pytest_gpu.log" 2>&1
   echo "exit=$?" >> "$OUT/pytest_gpu.log"
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
   echo "exit=$?" >> "$OUT/smoke.log"
 fi
 
-if [[ $WHAT == all || $WHAT == bench ]]; then
+if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
   echo "exit=$?" >> "$OUT/bench.err"
   timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
