@@ -110,6 +110,7 @@ struct tk_land {
     bool wide = false;
     tk::DevShape shape{};
     DevBuf pw, inm, odeg, flags, offsets, targets, minima, e_status, m_status, counter;
+    DevBuf om, tile_cnt, tile_base;  // staged two-pass build
     uint64_t n_edges = 0, n_minima = 0, n_strict = 0, n_ok = 0;
 
     DevBuf r0, r1, c0, c1, part;
@@ -240,8 +241,19 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     tk::StagePlan plan{};
     if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
         tk::make_stage_plan(s, false, l->smem_optin - 4096, &plan)) {
-        a.ntiles = static_cast<uint32_t>((n + plan.T - 1) / plan.T);  // staged tiles are T ranks
+        const uint32_t nt = static_cast<uint32_t>((n + plan.T - 1) / plan.T);  // T-rank tiles
+        a.ntiles = nt;
+        TKC(ensure(l->om, (n + kPad) * 4));
+        TKC(ensure(l->tile_cnt, static_cast<size_t>(nt) * 8 + 16));
+        TKC(ensure(l->tile_base, (static_cast<size_t>(nt) + 1) * 16));
+        a.om = l->om.as<uint32_t>();
+        a.tile_e = l->tile_cnt.as<uint32_t>();
+        a.tile_m = a.tile_e + nt;
+        a.ebase = l->tile_base.as<unsigned long long>();
+        a.mbase = a.ebase + (nt + 1);
         TKC(tk::launch_ffg_build_staged(s, plan, emit != 0, a, l->num_sms, l->stream));
+        TKC(cudaMemcpyAsync(ds->totals + 0, a.ebase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
+        TKC(cudaMemcpyAsync(ds->totals + 1, a.mbase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
         l->staged = true;
     } else {
         TKC(tk::launch_ffg_build(s, mode, wide, emit != 0, a, l->num_sms, l->stream));
@@ -524,6 +536,7 @@ int tk_land_destroy(tk_land* l) {
     DevBuf* bufs[] = {&l->fit, &l->ok, &l->hkeys, &l->hvals, &l->staging_keys, &l->staging_vals,
                       &l->staging_cfg, &l->pw, &l->inm, &l->odeg, &l->flags, &l->offsets,
                       &l->targets, &l->minima, &l->e_status, &l->m_status, &l->counter,
+                      &l->om, &l->tile_cnt, &l->tile_base,
                       &l->r0, &l->r1, &l->c0, &l->c1, &l->part, &l->small, &l->opt_part,
                       &l->cp_part, &l->cp_out, &l->tmp};
     for (DevBuf* b : bufs) b->release();

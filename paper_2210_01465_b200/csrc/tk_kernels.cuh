@@ -44,6 +44,12 @@ struct BuildArgs {
     unsigned int* tile_counter;
     unsigned long long* totals;   // [0] E, [1] M, [2] strict minima, [3] ok nodes
     uint32_t ntiles;
+    // two-pass staged build (count -> tile scan -> fill)
+    uint32_t* om;                 // canonical out-mask per rank
+    uint32_t* tile_e;             // per-tile edge count   (count pass)
+    uint32_t* tile_m;             // per-tile minima count (count pass)
+    unsigned long long* ebase;    // exclusive scan of tile_e, [ntiles] = E
+    unsigned long long* mbase;    // exclusive scan of tile_m, [ntiles] = M
 };
 constexpr int kBuildThreads = 256;
 cudaError_t launch_ffg_build(const DevShape& s, int mode, bool wide, bool emit,
@@ -127,6 +133,8 @@ struct StagePlan {
 };
 // kind_pr: PageRank layout (u32 pw[T], f64 r[T], window) vs FFG (u8 ok[T], window)
 bool make_stage_plan(const DevShape& s, bool kind_pr, int smem_budget, StagePlan* plan);
+// count (staged) -> tile scans -> fill; a.e_status/m_status/tile_counter are the
+// scan scratch (>= ceil(ntiles/256) tiles), totals[0..1] are written by the scan.
 cudaError_t launch_ffg_build_staged(const DevShape& s, const StagePlan& p, bool emit,
                                     const BuildArgs& a, int num_sms, cudaStream_t stream);
 cudaError_t launch_pagerank_staged(const DevShape& s, const StagePlan& p, const PrArgs& a,

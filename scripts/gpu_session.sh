@@ -27,20 +27,20 @@ if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
 fi
 
-if [[ $WHAT == all || $WHAT == ncu ]]; then
+if [[ $WHAT == all || $WHAT == ncu || $WHAT == quick ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu \
       > "$OUT/ncu_launches.log" 2>&1
   echo "exit=$?" >> "$OUT/ncu_launches.log"
   timeout 900 ncu --set full --clock-control none --import-source on \
-      -k regex:ffg_build_kernel -s 3 -c 1 -o "$OUT/prof_ffg" \
+      -k regex:ffg_ -s 3 -c 1 -o "$OUT/prof_ffg" \
       python bench.py --steps 1 --warmup 3 --no-cpu > "$OUT/ncu_ffg.log" 2>&1
   echo "exit=$?" >> "$OUT/ncu_ffg.log"
   timeout 1200 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis \
       --section LaunchStats --section Occupancy --section WarpStateStats --section SourceCounters \
       --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
       --clock-control none --import-source on \
-      -k regex:pagerank_kernel -s 3 -c 1 -o "$OUT/prof_pr" \
+      -k regex:pagerank -s 3 -c 1 -o "$OUT/prof_pr" \
       python bench.py --steps 1 --warmup 3 --no-cpu > "$OUT/ncu_pr.log" 2>&1
   echo "exit=$?" >> "$OUT/ncu_pr.log"
 fi
