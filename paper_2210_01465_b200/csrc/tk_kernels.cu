@@ -674,23 +674,40 @@ struct CpParams {
     int zero[TK_MAX_CP];
 };
 
-// blockIdx.y = p index; y == n_p accumulates the denominator (all minima).
+// One pass over the minima per block row: row y accumulates p = 16y .. 16y+15
+// in registers, row 0 also the denominator (stored at p index n_p).
+constexpr int kCpPerRow = 16;
 __global__ void __launch_bounds__(256) cp_partial_kernel(
     const uint32_t* __restrict__ minima, uint64_t m, const double* __restrict__ fit,
     const double* __restrict__ r, const CpParams P, double* __restrict__ part) {
     __shared__ double s_red[8];
-    const int p = blockIdx.y;
-    double acc = 0.0;
+    const int p0 = blockIdx.y * kCpPerRow;
+    double acc[kCpPerRow];
+#pragma unroll
+    for (int j = 0; j < kCpPerRow; ++j) acc[j] = 0.0;
+    double den = 0.0;
     for (uint64_t i = grid_stride_begin<uint64_t>(); i < m;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t idx = minima ? minima[i] : i;
-        const double f = fit[idx];
-        bool inc = true;
-        if (p < P.n_p) inc = P.zero[p] ? (f <= P.f_opt) : (f < P.thr[p]);
-        if (inc) acc = __dadd_rn(acc, r[idx]);
+        const uint64_t idx = minima ? __ldg(minima + i) : i;
+        const double f = __ldg(fit + idx);
+        const double pr = __ldg(r + idx);
+        den = __dadd_rn(den, pr);
+#pragma unroll
+        for (int j = 0; j < kCpPerRow; ++j) {
+            const int p = p0 + j;
+            if (p < P.n_p && (P.zero[p] ? (f <= P.f_opt) : (f < P.thr[p])))
+                acc[j] = __dadd_rn(acc[j], pr);
+        }
     }
-    acc = block_sum<256>(acc, s_red);
-    if (threadIdx.x == 0) part[static_cast<size_t>(p) * gridDim.x + blockIdx.x] = acc;
+#pragma unroll
+    for (int j = 0; j < kCpPerRow; ++j) {
+        const double s = block_sum<256>(acc[j], s_red);
+        if (threadIdx.x == 0 && p0 + j < P.n_p)
+            part[static_cast<size_t>(p0 + j) * gridDim.x + blockIdx.x] = s;
+    }
+    den = block_sum<256>(den, s_red);
+    if (threadIdx.x == 0 && blockIdx.y == 0)
+        part[static_cast<size_t>(P.n_p) * gridDim.x + blockIdx.x] = den;
 }
 
 __global__ void cp_final_kernel(const double* __restrict__ part, int n_p, int nblocks,
@@ -920,7 +937,7 @@ cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* 
         P.thr[i] = (1.0 + p[i]) * f_opt;  // host IEEE, same expression as the oracle
         P.zero[i] = p[i] == 0.0;
     }
-    dim3 grid(kCpBlocks, n_p + 1);
+    dim3 grid(kCpBlocks, (n_p + kCpPerRow - 1) / kCpPerRow);
     cp_partial_kernel<<<grid, 256, 0, stream>>>(minima, m, fit, r, P, part);
     cp_final_kernel<<<1, 128, 0, stream>>>(part, n_p, kCpBlocks, c_p_out, degenerate);
     return cudaGetLastError();
