@@ -126,6 +126,7 @@ struct tk_land {
     bool staged = false;                // last build used the TMA-staged kernel
     bool pr_staged = false;             // last PageRank used the TMA-staged kernel
     int pr_grid = 0;
+    bool opt_ready = false;  // small->f_opt/rank/has hold f_opt of the loaded table
 };
 
 namespace {
@@ -251,6 +252,13 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
         a.tile_m = a.tile_e + nt;
         a.ebase = l->tile_base.as<unsigned long long>();
         a.mbase = a.ebase + (nt + 1);
+        TKC(ensure(l->opt_part, static_cast<size_t>(l->num_sms) * 4 * 16));
+        a.opt_part_f = l->opt_part.as<double>();
+        a.opt_part_r = reinterpret_cast<unsigned long long*>(a.opt_part_f + l->num_sms * 4);
+        a.f_opt = &ds->f_opt;
+        a.opt_rank = &ds->rank;
+        a.opt_has = &ds->has;
+        l->opt_ready = true;
         TKC(tk::launch_ffg_build_staged(s, plan, emit != 0, a, l->num_sms, l->stream));
         TKC(cudaMemcpyAsync(ds->totals + 0, a.ebase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
         TKC(cudaMemcpyAsync(ds->totals + 1, a.mbase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
@@ -281,12 +289,15 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
 int do_optimum(tk_land* l, double* f_opt, uint64_t* rank) {
     if (!l->loaded) return fail(TK_ESTATE, "optimum: no fitness table loaded");
     TKC(set_dev(l));
-    TKC(ensure(l->opt_part, 148 * 4 * 16));
     Small* ds = l->small.as<Small>();
-    TKC(tk::launch_optimum(l->fit.as<double>(), l->ok.as<uint8_t>(), static_cast<uint32_t>(l->n),
-                           l->opt_part.as<double>(),
-                           reinterpret_cast<unsigned long long*>(l->opt_part.as<double>() + 148 * 4),
-                           &ds->f_opt, &ds->rank, &ds->has, l->stream));
+    if (!l->opt_ready) {  // the staged FFG count pass already reduced it otherwise
+        TKC(ensure(l->opt_part, 148 * 4 * 16));
+        TKC(tk::launch_optimum(l->fit.as<double>(), l->ok.as<uint8_t>(),
+                               static_cast<uint32_t>(l->n), l->opt_part.as<double>(),
+                               reinterpret_cast<unsigned long long*>(l->opt_part.as<double>() + 148 * 4),
+                               &ds->f_opt, &ds->rank, &ds->has, l->stream));
+        l->opt_ready = true;
+    }
     TKC(cudaMemcpyAsync(&l->hsmall->f_opt, &ds->f_opt, 8 + 8 + 4, cudaMemcpyDeviceToHost,
                         l->stream));
     TKC(cudaStreamSynchronize(l->stream));
@@ -441,6 +452,7 @@ int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const doubl
         return fail(TK_EINVAL, "load: duplicate configuration key");
     }
     l->loaded = true;
+    l->opt_ready = false;
     return TK_OK;
 }
 
@@ -578,6 +590,7 @@ int tk_land_load_dense(tk_land* l, const double* fitness, const uint8_t* ok, int
     TKC(cudaMemcpyAsync(l->ok.p, ok, l->n, h2x(mem), l->stream));
     TKC(cudaStreamSynchronize(l->stream));
     l->loaded = true;
+    l->opt_ready = false;
     l->built = l->pr_done = false;
     return TK_OK;
 }
@@ -649,6 +662,7 @@ int tk_land_generate(tk_land* l, int gen, double fail_fraction, uint64_t seed) {
                             l->fit.as<double>(), l->ok.as<uint8_t>(), l->stream));
     TKC(cudaStreamSynchronize(l->stream));
     l->loaded = true;
+    l->opt_ready = false;
     l->built = l->pr_done = false;
     return TK_OK;
 }

@@ -809,6 +809,13 @@ cudaError_t launch_optimum(const double* fit, const uint8_t* ok, uint32_t n, dou
     return cudaGetLastError();
 }
 
+cudaError_t launch_optimum_final(const double* part_f, const unsigned long long* part_r,
+                                 int nparts, double* f_opt, unsigned long long* rank, int* has,
+                                 cudaStream_t stream) {
+    optimum_final_kernel<<<1, 256, 0, stream>>>(part_f, part_r, nparts, f_opt, rank, has);
+    return cudaGetLastError();
+}
+
 template <int KIND, typename MW, bool PACKED, bool EMIT>
 static cudaError_t build_one(const DevShape& s, const BuildArgs& a, int num_sms,
                              cudaStream_t stream) {

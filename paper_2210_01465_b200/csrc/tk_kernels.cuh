@@ -27,6 +27,10 @@ cudaError_t launch_hash_lookup(const unsigned long long* hkeys, const double* hv
 cudaError_t launch_optimum(const double* fit, const uint8_t* ok, uint32_t n,
                            double* part_f, unsigned long long* part_r, double* f_opt,
                            unsigned long long* rank, int* has, cudaStream_t stream);
+// final argmin over nparts (fitness, rank) partials (rank ~0 = empty partial)
+cudaError_t launch_optimum_final(const double* part_f, const unsigned long long* part_r,
+                                 int nparts, double* f_opt, unsigned long long* rank, int* has,
+                                 cudaStream_t stream);
 
 // ---- FFG ---------------------------------------------------------------------
 struct BuildArgs {
@@ -50,6 +54,12 @@ struct BuildArgs {
     uint32_t* tile_m;             // per-tile minima count (count pass)
     unsigned long long* ebase;    // exclusive scan of tile_e, [ntiles] = E
     unsigned long long* mbase;    // exclusive scan of tile_m, [ntiles] = M
+    // f_opt fused into the count pass: per-block (fitness, rank) argmin over ok ranks
+    double* opt_part_f;
+    unsigned long long* opt_part_r;
+    double* f_opt;                // final reduction target (device)
+    unsigned long long* opt_rank;
+    int* opt_has;
 };
 constexpr int kBuildThreads = 256;
 cudaError_t launch_ffg_build(const DevShape& s, int mode, bool wide, bool emit,
