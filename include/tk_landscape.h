@@ -148,6 +148,35 @@ int tk_analyze(tk_land* land, int kind, double damping, double tol, int64_t max_
                uint64_t node_limit, int p_max_percent, int emit_csr,
                tk_report_summary* out);
 
+/* ------------------------------------- key-range sharding -- */
+/* Multi-GPU analyze_landscape: one handle per GPU, every handle loads the full
+ * fitness table, handle `rank` of `nranks` owns ranks [lo, hi) (lo = rank *
+ * chunk, chunk = ceil(N/nranks) rounded up to 512).  Adjacent spaces with
+ * 2*dims <= 27 only.  After tk_land_set_shard, tk_ffg_build builds the
+ * shard's rows only (n_edges / n_minima are the shard's counts, no CSR).
+ * The host sums the per-shard partials across ranks between calls (see
+ * paper_2210_01465_b200/sharded.py); that reduction is the iteration barrier. */
+int tk_land_set_shard(tk_land* land, int rank, int nranks, uint64_t* lo, uint64_t* hi);
+/* device pointers of this handle's two PageRank contribution replicas */
+int tk_land_replica_ptrs(tk_land* land, void** c0, void** c1);
+/* peers' replicas (nranks entries each, own entry ignored): same process */
+int tk_land_set_peer_ptrs(tk_land* land, void* const* c0, void* const* c1);
+/* the replicas as two cudaIpcMemHandle_t (128 bytes); tk_land_open_peers maps
+ * the nranks*128 bytes of every rank's handles (own entry ignored) */
+int tk_land_ipc_handles(tk_land* land, void* handles128);
+int tk_land_open_peers(tk_land* land, const void* handles);
+/* shard partials: (fitness, rank) minimum over the shard's ok ranks; has = 0 if none */
+int tk_shard_optimum(tk_land* land, double* f, uint64_t* rank, int* has);
+int tk_shard_pagerank_init(tk_land* land, double damping, double* dangling);
+/* one iteration: dangling_total = summed dangling mass of the previous iterate */
+int tk_shard_pagerank_step(tk_land* land, double dangling_total, double damping,
+                           double* residual, double* dangling, double* sum);
+/* nums[n_p] and den: the shard's C_p numerators / denominator */
+int tk_shard_centrality(tk_land* land, double f_opt, const double* p, int n_p, double* nums,
+                        double* den);
+/* the shard's slice [lo, hi) of the current rank vector */
+int tk_shard_pagerank_copy_out(tk_land* land, double* r_slice);
+
 /* ---------------------------------------------- free-standing (host CSR) -- */
 
 /* pagerank(const FitnessFlowGraph&) (landscape.hpp:51-52) for an arbitrary

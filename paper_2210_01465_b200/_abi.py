@@ -28,6 +28,9 @@ EXPORTS = [
     "tk_ffg_build", "tk_ffg_copy_out", "tk_census", "tk_pagerank",
     "tk_pagerank_copy_out", "tk_centrality", "tk_report_copy_out", "tk_analyze",
     "tk_pagerank_csr", "tk_proportion_of_centrality",
+    "tk_land_set_shard", "tk_land_replica_ptrs", "tk_land_set_peer_ptrs", "tk_land_ipc_handles",
+    "tk_land_open_peers", "tk_shard_optimum", "tk_shard_pagerank_init", "tk_shard_pagerank_step",
+    "tk_shard_centrality", "tk_shard_pagerank_copy_out",
 ]
 
 
@@ -84,6 +87,16 @@ def load(path: str = LIB_PATH):
         "tk_analyze": (I, [P, I, D, D, C.c_int64, U64, I, I, C.POINTER(ReportSummary)]),
         "tk_pagerank_csr": (I, [I, U64, P, P, D, D, C.c_int64, P, PI64, PD]),
         "tk_proportion_of_centrality": (I, [I, U64, P, P, D, D, PD]),
+        "tk_land_set_shard": (I, [P, I, I, PU64, PU64]),
+        "tk_land_replica_ptrs": (I, [P, C.POINTER(P), C.POINTER(P)]),
+        "tk_land_set_peer_ptrs": (I, [P, P, P]),
+        "tk_land_ipc_handles": (I, [P, P]),
+        "tk_land_open_peers": (I, [P, P]),
+        "tk_shard_optimum": (I, [P, PD, PU64, C.POINTER(I)]),
+        "tk_shard_pagerank_init": (I, [P, D, PD]),
+        "tk_shard_pagerank_step": (I, [P, D, D, PD, PD, PD]),
+        "tk_shard_centrality": (I, [P, D, P, I, P, PD]),
+        "tk_shard_pagerank_copy_out": (I, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -87,6 +87,7 @@ struct Small {  // device-side scalars read back by the host
     int degenerate;
     int pad;
     PrOut pr;
+    double totals_f[3];  // shard PageRank partials (residual, dangling, sum)
 };
 
 }  // namespace
@@ -127,6 +128,16 @@ struct tk_land {
     bool pr_staged = false;             // last PageRank used the TMA-staged kernel
     int pr_grid = 0;
     bool opt_ready = false;  // small->f_opt/rank/has hold f_opt of the loaded table
+
+    // key-range sharding (tk_land_set_shard)
+    bool sharded = false;
+    int shard_rank = 0, shard_n = 1;
+    uint64_t shard_lo = 0, shard_hi = 0, shard_chunk = 0;
+    void* peer_c0[tk::kMaxShards] = {};
+    void* peer_c1[tk::kMaxShards] = {};
+    std::vector<void*> ipc_opened;
+    int shard_cur = 0;          // parity holding the current iterate
+    bool shard_pr = false;      // tk_shard_pagerank_init done
 };
 
 namespace {
@@ -242,8 +253,16 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     tk::StagePlan plan{};
     if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
         tk::make_stage_plan(s, false, l->smem_optin - 4096, &plan)) {
-        const uint32_t nt = static_cast<uint32_t>((n + plan.T - 1) / plan.T);  // T-rank tiles
+        // T-rank tiles over the whole space, or over this handle's shard
+        const uint64_t lo = l->sharded ? l->shard_lo : 0, hi = l->sharded ? l->shard_hi : n;
+        const uint32_t nt = static_cast<uint32_t>((hi - lo + plan.T - 1) / plan.T);
         a.ntiles = nt;
+        a.tile_lo = static_cast<uint32_t>(lo / plan.T);
+        if (l->sharded) {
+            a.offsets = nullptr;
+            a.targets = nullptr;
+            emit = 0;
+        }
         TKC(ensure(l->om, (n + kPad) * 4));
         TKC(ensure(l->tile_cnt, static_cast<size_t>(nt) * 8 + 16));
         TKC(ensure(l->tile_base, (static_cast<size_t>(nt) + 1) * 16));
@@ -264,6 +283,9 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
         TKC(cudaMemcpyAsync(ds->totals + 1, a.mbase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
         l->staged = true;
     } else {
+        if (l->sharded)
+            return fail(TK_EINVAL, "sharded builds need an Adjacent space with 2*dims <= 27 "
+                                   "(the TMA-staged path)");
         TKC(tk::launch_ffg_build(s, mode, wide, emit != 0, a, l->num_sms, l->stream));
         l->staged = false;
     }
@@ -545,6 +567,7 @@ int tk_land_destroy(tk_land* l) {
     if (!l) return TK_OK;
     cudaSetDevice(l->device);
     if (l->stream) cudaStreamSynchronize(l->stream);
+    for (void* p : l->ipc_opened) cudaIpcCloseMemHandle(p);
     DevBuf* bufs[] = {&l->fit, &l->ok, &l->hkeys, &l->hvals, &l->staging_keys, &l->staging_vals,
                       &l->staging_cfg, &l->pw, &l->inm, &l->odeg, &l->flags, &l->offsets,
                       &l->targets, &l->minima, &l->e_status, &l->m_status, &l->counter,
@@ -858,6 +881,219 @@ int tk_analyze(tk_land* l, int kind, double damping, double tol, int64_t max_ite
     TKC(cudaEventElapsedTime(&out->ms_centrality, l->ev[4], l->ev[5]));
     return TK_OK;
     TK_GUARD_END
+}
+
+// ------------------------------------------------ key-range sharding ABI --
+
+int tk_land_set_shard(tk_land* l, int rank, int nranks, uint64_t* lo, uint64_t* hi) {
+    if (int st = check_land(l)) return st;
+    if (nranks < 1 || nranks > tk::kMaxShards || rank < 0 || rank >= nranks)
+        return fail(TK_EINVAL, "set_shard: need 0 <= rank < nranks <= 8");
+    uint64_t chunk = (l->n + nranks - 1) / nranks;
+    chunk = (chunk + 511) / 512 * 512;
+    l->shard_rank = rank;
+    l->shard_n = nranks;
+    l->shard_chunk = chunk;
+    l->shard_lo = std::min<uint64_t>(l->n, static_cast<uint64_t>(rank) * chunk);
+    l->shard_hi = std::min<uint64_t>(l->n, l->shard_lo + chunk);
+    l->sharded = true;
+    l->built = l->pr_done = l->shard_pr = false;
+    TKC(set_dev(l));
+    TKC(ensure(l->c0, (l->n + kPad) * 8));  // replicas exist before peers map them
+    TKC(ensure(l->c1, (l->n + kPad) * 8));
+    for (int g = 0; g < tk::kMaxShards; ++g) l->peer_c0[g] = l->peer_c1[g] = nullptr;
+    l->peer_c0[rank] = l->c0.p;
+    l->peer_c1[rank] = l->c1.p;
+    if (lo) *lo = l->shard_lo;
+    if (hi) *hi = l->shard_hi;
+    return TK_OK;
+}
+
+int tk_land_replica_ptrs(tk_land* l, void** c0, void** c1) {
+    if (int st = check_land(l)) return st;
+    if (!l->sharded) return fail(TK_ESTATE, "replica_ptrs: call tk_land_set_shard first");
+    if (c0) *c0 = l->c0.p;
+    if (c1) *c1 = l->c1.p;
+    return TK_OK;
+}
+
+int tk_land_set_peer_ptrs(tk_land* l, void* const* c0, void* const* c1) {
+    if (int st = check_land(l)) return st;
+    if (!l->sharded) return fail(TK_ESTATE, "set_peer_ptrs: call tk_land_set_shard first");
+    for (int g = 0; g < l->shard_n; ++g) {
+        if (g == l->shard_rank) continue;
+        if (!c0[g] || !c1[g]) return fail(TK_EINVAL, "set_peer_ptrs: null replica pointer");
+        l->peer_c0[g] = c0[g];
+        l->peer_c1[g] = c1[g];
+    }
+    return TK_OK;
+}
+
+int tk_land_ipc_handles(tk_land* l, void* handles128) {
+    if (int st = check_land(l)) return st;
+    if (!l->sharded) return fail(TK_ESTATE, "ipc_handles: call tk_land_set_shard first");
+    TKC(set_dev(l));
+    cudaIpcMemHandle_t h[2];
+    TKC(cudaIpcGetMemHandle(&h[0], l->c0.p));
+    TKC(cudaIpcGetMemHandle(&h[1], l->c1.p));
+    std::memcpy(handles128, h, sizeof h);
+    return TK_OK;
+}
+
+int tk_land_open_peers(tk_land* l, const void* handles) {
+    if (int st = check_land(l)) return st;
+    if (!l->sharded) return fail(TK_ESTATE, "open_peers: call tk_land_set_shard first");
+    TKC(set_dev(l));
+    const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+    for (int g = 0; g < l->shard_n; ++g) {
+        if (g == l->shard_rank) continue;
+        void* p0 = nullptr;
+        void* p1 = nullptr;
+        TKC(cudaIpcOpenMemHandle(&p0, h[2 * g], cudaIpcMemLazyEnablePeerAccess));
+        l->ipc_opened.push_back(p0);
+        TKC(cudaIpcOpenMemHandle(&p1, h[2 * g + 1], cudaIpcMemLazyEnablePeerAccess));
+        l->ipc_opened.push_back(p1);
+        l->peer_c0[g] = p0;
+        l->peer_c1[g] = p1;
+    }
+    return TK_OK;
+}
+
+namespace {
+int shard_ready(tk_land* l) {
+    if (!l->sharded) return fail(TK_ESTATE, "shard call on an unsharded handle");
+    if (!l->built || !l->staged) return fail(TK_ESTATE, "shard call before tk_ffg_build");
+    for (int g = 0; g < l->shard_n; ++g)
+        if (!l->peer_c0[g] || !l->peer_c1[g])
+            return fail(TK_ESTATE, "shard peers not connected (tk_land_set_peer_ptrs / open_peers)");
+    return TK_OK;
+}
+
+tk::ShardInfo shard_info(const tk_land* l) {
+    tk::ShardInfo sh{};
+    sh.nranks = l->shard_n;
+    sh.self = l->shard_rank;
+    sh.lo = static_cast<uint32_t>(l->shard_lo);
+    sh.hi = static_cast<uint32_t>(l->shard_hi);
+    sh.chunk_magic = l->shard_chunk == 1 ? 0ull : (~0ull / l->shard_chunk + 1ull);
+    for (int g = 0; g < l->shard_n; ++g) {
+        sh.peer_c[0][g] = static_cast<double*>(l->peer_c0[g]);
+        sh.peer_c[1][g] = static_cast<double*>(l->peer_c1[g]);
+    }
+    return sh;
+}
+
+tk::PrArgs shard_pr_args(tk_land* l, double d) {
+    tk::PrArgs a{};
+    a.n = static_cast<uint32_t>(l->n);
+    const double nd = static_cast<double>(l->n);
+    a.inv_n = 1.0 / nd;
+    a.nd = nd;
+    a.teleport = (1.0 - d) / nd;
+    a.damping = d;
+    a.pw = l->pw.as<uint32_t>();
+    a.r0 = l->r0.as<double>();
+    a.r1 = l->r1.as<double>();
+    a.c0 = l->c0.as<double>();
+    a.c1 = l->c1.as<double>();
+    return a;
+}
+}  // namespace
+
+int tk_shard_optimum(tk_land* l, double* f, uint64_t* rank, int* has) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    TKC(set_dev(l));
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemcpyAsync(&l->hsmall->f_opt, &ds->f_opt, 8 + 8 + 4, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    if (f) *f = l->hsmall->f_opt;
+    if (rank) *rank = l->hsmall->rank;
+    if (has) *has = l->hsmall->has;
+    return TK_OK;
+}
+
+int tk_shard_pagerank_init(tk_land* l, double damping, double* dangling) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    if (int st = check_pr_args(damping, 1.0, 1)) return st;
+    TKC(set_dev(l));
+    TKC(ensure(l->r0, (l->n + kPad) * 8));
+    TKC(ensure(l->r1, (l->n + kPad) * 8));
+    TKC(ensure(l->part, static_cast<size_t>(l->num_sms) * 4 * 3 * 8));
+    Small* ds = l->small.as<Small>();
+    tk::PrArgs a = shard_pr_args(l, damping);
+    TKC(tk::launch_pagerank_shard_init(l->shape, shard_info(l), a, l->om.as<uint32_t>(),
+                                       l->part.as<double>(), ds->totals_f, l->num_sms, l->stream));
+    TKC(cudaMemcpyAsync(l->hsmall->totals_f, ds->totals_f, 24, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    if (dangling) *dangling = l->hsmall->totals_f[1];
+    l->shard_cur = 0;
+    l->shard_pr = true;
+    l->iterations = 0;
+    return TK_OK;
+}
+
+int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, double* residual,
+                           double* dangling, double* sum) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    if (!l->shard_pr) return fail(TK_ESTATE, "shard step before tk_shard_pagerank_init");
+    TKC(set_dev(l));
+    tk::StagePlan plan{};
+    if (!tk::make_stage_plan(l->shape, true, l->smem_optin - 4096, &plan))
+        return fail(TK_EINVAL, "shard step: no staging plan for this shape");
+    Small* ds = l->small.as<Small>();
+    tk::PrArgs a = shard_pr_args(l, damping);
+    const double dn = dangling_total / static_cast<double>(l->n);
+    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a, l->om.as<uint32_t>(),
+                                       l->shard_cur, dn, l->part.as<double>(), ds->totals_f,
+                                       l->num_sms, l->stream));
+    TKC(cudaMemcpyAsync(l->hsmall->totals_f, ds->totals_f, 24, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->shard_cur ^= 1;
+    ++l->iterations;
+    if (residual) *residual = l->hsmall->totals_f[0];
+    if (dangling) *dangling = l->hsmall->totals_f[1];
+    if (sum) *sum = l->hsmall->totals_f[2];
+    return TK_OK;
+}
+
+int tk_shard_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* nums,
+                        double* den) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    if (!l->shard_pr) return fail(TK_ESTATE, "shard centrality before PageRank");
+    if (n_p < 1 || n_p > TK_MAX_CP) return fail(TK_EINVAL, "centrality: 1..101 values of p");
+    TKC(set_dev(l));
+    if (l->n_minima == 0) {
+        for (int k = 0; k < n_p; ++k) nums[k] = 0.0;
+        *den = 0.0;
+        return TK_OK;
+    }
+    TKC(ensure(l->cp_part, static_cast<size_t>(TK_MAX_CP + 1) * tk::kCpBlocks * 8));
+    TKC(ensure(l->cp_out, (TK_MAX_CP + 1) * 8));
+    Small* ds = l->small.as<Small>();
+    const double* r = l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
+    TKC(tk::launch_centrality(l->minima.as<uint32_t>(), l->n_minima, l->fit.as<double>(), r, p, n_p,
+                              f_opt, l->cp_part.as<double>(), l->cp_out.as<double>(),
+                              &ds->degenerate, l->stream, true));
+    TKC(cudaMemcpyAsync(nums, l->cp_out.p, static_cast<size_t>(n_p) * 8, cudaMemcpyDeviceToHost,
+                        l->stream));
+    TKC(cudaMemcpyAsync(den, l->cp_out.as<double>() + n_p, 8, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
+}
+
+int tk_shard_pagerank_copy_out(tk_land* l, double* r_slice) {
+    if (int st = check_land(l)) return st;
+    if (!l->sharded || !l->shard_pr) return fail(TK_ESTATE, "no sharded PageRank state");
+    TKC(set_dev(l));
+    const double* r = l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
+    TKC(cudaMemcpyAsync(r_slice, r + l->shard_lo, (l->shard_hi - l->shard_lo) * 8,
+                        cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    return TK_OK;
 }
 
 int tk_pagerank_csr(int device, uint64_t n, const uint64_t* offsets, const uint32_t* targets,

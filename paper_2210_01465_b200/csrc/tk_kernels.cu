@@ -710,20 +710,23 @@ __global__ void __launch_bounds__(256) cp_partial_kernel(
         part[static_cast<size_t>(P.n_p) * gridDim.x + blockIdx.x] = den;
 }
 
+// raw = 1 writes the sums (n_p numerators, then the denominator) instead of
+// the ratios: a shard's partials for the cross-GPU sum.
 __global__ void cp_final_kernel(const double* __restrict__ part, int n_p, int nblocks,
-                                double* __restrict__ c_p, int* degenerate) {
+                                double* __restrict__ c_p, int* degenerate, int raw) {
     __shared__ double s_den;
     if (threadIdx.x == 0) {
         double den = 0.0;
         for (int b = 0; b < nblocks; ++b) den = __dadd_rn(den, part[static_cast<size_t>(n_p) * nblocks + b]);
         s_den = den;
         *degenerate = !(den > 0.0);
+        if (raw) c_p[n_p] = den;
     }
     __syncthreads();
     for (int p = threadIdx.x; p < n_p; p += blockDim.x) {
         double num = 0.0;
         for (int b = 0; b < nblocks; ++b) num = __dadd_rn(num, part[static_cast<size_t>(p) * nblocks + b]);
-        c_p[p] = __ddiv_rn(num, s_den);
+        c_p[p] = raw ? num : __ddiv_rn(num, s_den);
     }
 }
 
@@ -936,7 +939,7 @@ cudaError_t launch_pagerank(const DevShape& s, int mode, bool wide, const PrArgs
 cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* fit,
                               const double* r, const double* p, int n_p, double f_opt,
                               double* part, double* c_p_out, int* degenerate,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, bool raw) {
     CpParams P{};
     P.n_p = n_p;
     P.f_opt = f_opt;
@@ -946,7 +949,7 @@ cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* 
     }
     dim3 grid(kCpBlocks, (n_p + kCpPerRow - 1) / kCpPerRow);
     cp_partial_kernel<<<grid, 256, 0, stream>>>(minima, m, fit, r, P, part);
-    cp_final_kernel<<<1, 128, 0, stream>>>(part, n_p, kCpBlocks, c_p_out, degenerate);
+    cp_final_kernel<<<1, 128, 0, stream>>>(part, n_p, kCpBlocks, c_p_out, degenerate, raw ? 1 : 0);
     return cudaGetLastError();
 }
 

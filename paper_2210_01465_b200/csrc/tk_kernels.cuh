@@ -60,6 +60,18 @@ struct BuildArgs {
     double* f_opt;                // final reduction target (device)
     unsigned long long* opt_rank;
     int* opt_has;
+    uint32_t tile_lo;             // first tile of this shard (0 unsharded)
+};
+
+// Key-range shard of a multi-GPU run: this device owns ranks
+// [lo, hi); c replicas of every rank (own included) for both parities.
+constexpr int kMaxShards = 8;
+struct ShardInfo {
+    int nranks;          // 1 = unsharded
+    int self;
+    uint32_t lo, hi;
+    unsigned long long chunk_magic;  // fdiv magic of the chunk length
+    double* peer_c[2][kMaxShards];   // [parity][rank] replica base pointers
 };
 constexpr int kBuildThreads = 256;
 cudaError_t launch_ffg_build(const DevShape& s, int mode, bool wide, bool emit,
@@ -149,14 +161,27 @@ cudaError_t launch_ffg_build_staged(const DevShape& s, const StagePlan& p, bool 
                                     const BuildArgs& a, int num_sms, cudaStream_t stream);
 cudaError_t launch_pagerank_staged(const DevShape& s, const StagePlan& p, const PrArgs& a,
                                    int num_sms, int* grid_out, cudaStream_t stream);
+// Shard steps (one launch per PageRank iteration, no grid barrier): ranks
+// [sh.lo, sh.hi); c' is stored into the local replica and, for ranks with an
+// out-neighbour owned by another shard, into that shard's replica.
+// init: r0, c0 (parity 0) + dangling partial;  step: reads parity `cur`,
+// writes parity cur^1.  Partials land in out3[0..2] (res, dangling, sum).
+cudaError_t launch_pagerank_shard_init(const DevShape& s, const ShardInfo& sh, const PrArgs& a,
+                                       const uint32_t* om, double* part, double* out3,
+                                       int num_sms, cudaStream_t stream);
+cudaError_t launch_pagerank_shard_step(const DevShape& s, const StagePlan& p, const ShardInfo& sh,
+                                       const PrArgs& a, const uint32_t* om, int cur, double dn,
+                                       double* part, double* out3, int num_sms,
+                                       cudaStream_t stream);
 
 // ---- C_p and report -------------------------------------------------------
 constexpr int kCpBlocks = 148;
 // minima == nullptr: fit/r are already per-minimum arrays of length m.
+// raw: c_p_out receives n_p numerators then the denominator (n_p + 1 values).
 cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* fit,
                               const double* r, const double* p, int n_p, double f_opt,
                               double* part, double* c_p_out, int* degenerate,
-                              cudaStream_t stream);
+                              cudaStream_t stream, bool raw = false);
 cudaError_t launch_report(const uint32_t* minima, uint64_t m, const double* fit,
                           const double* r, double f_opt, unsigned long long* ranks,
                           double* fitness, double* fraction, double* pr,

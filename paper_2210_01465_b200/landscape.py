@@ -327,6 +327,60 @@ class Landscape:
                                          _ptr(pr)))
         return ranks, fit, frac, pr
 
+    # ---- key-range sharding (sharded.py drives these)
+    def set_shard(self, rank: int, nranks: int):
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _check(self.L.tk_land_set_shard(self.h, rank, nranks, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def replica_ptrs(self):
+        c0, c1 = C.c_void_p(), C.c_void_p()
+        _check(self.L.tk_land_replica_ptrs(self.h, C.byref(c0), C.byref(c1)))
+        return c0.value, c1.value
+
+    def set_peer_ptrs(self, ptrs):
+        arr0 = (C.c_void_p * len(ptrs))(*[p[0] for p in ptrs])
+        arr1 = (C.c_void_p * len(ptrs))(*[p[1] for p in ptrs])
+        _check(self.L.tk_land_set_peer_ptrs(self.h, arr0, arr1))
+
+    def ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(self.L.tk_land_ipc_handles(self.h, buf))
+        return buf.raw
+
+    def open_peers(self, handles):
+        blob = b"".join(handles)
+        _check(self.L.tk_land_open_peers(self.h, C.create_string_buffer(blob, len(blob))))
+
+    def shard_optimum(self):
+        f, r, has = C.c_double(), C.c_uint64(), C.c_int()
+        _check(self.L.tk_shard_optimum(self.h, C.byref(f), C.byref(r), C.byref(has)))
+        return f.value, r.value, bool(has.value)
+
+    def shard_pagerank_init(self, damping):
+        d = C.c_double()
+        _check(self.L.tk_shard_pagerank_init(self.h, damping, C.byref(d)))
+        return d.value
+
+    def shard_pagerank_step(self, dangling, damping):
+        r, d, s = C.c_double(), C.c_double(), C.c_double()
+        _check(self.L.tk_shard_pagerank_step(self.h, dangling, damping, C.byref(r), C.byref(d),
+                                             C.byref(s)))
+        return r.value, d.value, s.value
+
+    def shard_centrality(self, f_opt, ps):
+        p = np.ascontiguousarray(ps, np.float64)
+        nums = np.zeros(p.shape[0], np.float64)
+        den = C.c_double()
+        _check(self.L.tk_shard_centrality(self.h, f_opt, _ptr(p), p.shape[0], _ptr(nums),
+                                          C.byref(den)))
+        return nums, den.value
+
+    def shard_pagerank_vector(self, lo, hi):
+        r = np.empty(hi - lo, np.float64)
+        _check(self.L.tk_shard_pagerank_copy_out(self.h, _ptr(r)))
+        return r
+
     def analyze(self, kind: int, damping=0.85, tol=1e-10, max_iter=100000,
                 node_limit=1_000_000, p_max_percent=15, emit_csr=False):
         s = _abi.ReportSummary()
