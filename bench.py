@@ -12,10 +12,12 @@ inside the timed region, minima report D2H after it).
 GTEPS = E * (iterations + 1) / t_step / 1e9: the FFG build traverses every
 edge once and each PageRank iteration once more.
 
-Multi-GPU (torchrun, one process per GPU): N independent replicas of the
-workload, one per GPU ("scaling": "weak"); value = all edges traversed on all
-ranks / max-over-ranks time.  (Key-range sharding of one space across GPUs
-with a rank-vector exchange is DESIGN.md's next step.)
+Multi-GPU (torchrun, one process per GPU): the one space is key-range
+sharded, one shard per GPU (paper_2210_01465_b200/sharded.py): each PageRank
+iteration pushes the contributions a peer pulls into that peer's replica over
+NVLink from inside the step kernel, and the per-shard partial sums are
+all-reduced with NCCL.  Total work is fixed ("scaling": "strong"); time is the
+max over ranks.
 """
 from __future__ import annotations
 
@@ -324,6 +326,126 @@ def run_b200(args, wl, kind):
     return 0
 
 
+def run_sharded(args, wl, kind):
+    """N GPUs (torchrun): the space is key-range sharded, one shard per GPU;
+    each PageRank iteration pushes the new contributions a peer pulls into that
+    peer's replica over NVLink from inside the step kernel, and the per-shard
+    partials are all-reduced (NCCL) -- the iteration barrier.  Strong scaling:
+    the total work (one C5 space) is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    # TK_FORCE_DEVICE / TK_DIST_BACKEND=gloo let the multi-process path run with
+    # several ranks on one GPU (CUDA IPC still maps the peers' replicas)
+    local = int(os.environ.get("TK_FORCE_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    backend = os.environ.get("TK_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    from paper_2210_01465_b200 import sharded as S
+
+    radix = wl["radix"]
+    shard = S.GpuShard(radix, rank, world, device=local)
+    shard.land.generate(wl["gen"], wl["q"], wl["seed"])  # read-only table, replicated
+    allreduce, allgather = S.torch_collectives(device=f"cuda:{local}")
+    S.connect_peers_ipc(shard, allgather)
+    stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device("cuda", local))
+
+    def step():
+        return S.analyze_sharded([shard], allreduce, allgather, kind, DAMPING, TOL, MAX_ITER,
+                                 P_MAX)
+
+    for _ in range(max(3, args.warmup)):
+        res = step()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    clocks.start()
+    ev0.record(stream)
+    t0 = time.perf_counter()
+    runs = [step() for _ in range(args.steps)]
+    ev1.record(stream)
+    ev1.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3
+    clk = clocks.stop()
+    t = torch.tensor([max(ev0.elapsed_time(ev1), wall)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+
+    # e2e: every rank uploads the fitness table from pinned host memory, runs the
+    # sharded analysis and reads its minima report rows back
+    import ctypes as C
+
+    f_np, o_np = shard.land.fitness()
+    fit_h = torch.empty(shard.land.n, dtype=torch.float64, pin_memory=True)
+    ok_h = torch.empty(shard.land.n, dtype=torch.uint8, pin_memory=True)
+    fit_h.numpy()[:] = f_np
+    ok_h.numpy()[:] = o_np
+    m_local = shard.land.n_minima
+    rep = [torch.empty(max(1, m_local), dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    L = shard.land.L
+
+    def e2e_step():
+        assert L.tk_land_load_dense(shard.land.h, C.c_void_p(fit_h.data_ptr()),
+                                    C.c_void_p(ok_h.data_ptr()), 0) == 0
+        r = step()
+        assert L.tk_report_copy_out(shard.land.h, r["f_opt"], *[C.c_void_p(x.data_ptr())
+                                                                for x in rep]) == 0
+        return r
+
+    e2e_step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2e_runs = [e2e_step() for _ in range(args.steps)]
+    torch.cuda.synchronize(local)
+    t = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64,
+                     device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_e2e = float(t.item())
+    e2e_value = sum(x["n_edges"] * (x["iterations"] + 1) for x in e2e_runs) / (t_e2e / 1e3) / 1e9
+    e = runs[-1]["n_edges"]
+    value = sum(e * (r["iterations"] + 1) for r in runs) / (t_ms / 1e3) / 1e9
+    n = shard.land.n
+    it = runs[-1]["iterations"]
+    peaks, peak_src = measured_peaks()
+    per_gpu_bytes = (20 * n + 36 * n * it) / world  # PageRank algorithmic bytes per GPU
+    ms_step = t_ms / args.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": "FFG+PageRank GTEPS", "value": round(value, 3), "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"],
+                       "nodes": n, "edges": e, "minima": runs[-1]["n_minima"],
+                       "pagerank_iterations": it, "parallelism": f"keyrange{world}",
+                       "l2": "inputs larger than L2"},
+            "s_per_space": round(ms_step / 1e3, 5),
+            "roofline": {"bound": "hbm", "achieved": round(per_gpu_bytes / (ms_step / 1e3) / 1e9, 1),
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(per_gpu_bytes / (ms_step / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": "whole sharded step (per GPU)"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": 9 * n * world,
+                    "d2h_bytes_per_step": 32 * runs[-1]["n_minima"],
+                    "ms_per_step": round(t_e2e / args.steps, 3)},
+            "gpu_launches": args.steps * (4 + 2 * (it + 1) + 2),
+            "clocks": clk,
+        }))
+    shard.land.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def land_mode_packed(radix, kind) -> bool:
     dims = sum(1 for m in radix if m >= 2)
     return kind == 1 and 2 * dims <= 27
@@ -343,6 +465,8 @@ def main() -> int:
     kind = KIND[args.kind]
     if args.impl == "reference":
         return run_reference(args, wl, kind)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_sharded(args, wl, kind)
     return run_b200(args, wl, kind)
 
 

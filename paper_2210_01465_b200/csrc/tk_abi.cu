@@ -305,6 +305,7 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     l->built = true;
     l->emitted = emit != 0;
     l->pr_done = false;
+    l->shard_pr = false;
     return TK_OK;
 }
 
@@ -417,6 +418,7 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
 }
 
 const double* pr_result(const tk_land* l) {
+    if (l->sharded && l->shard_pr) return l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
     return l->pr_parity ? l->r1.as<double>() : l->r0.as<double>();
 }
 
@@ -820,7 +822,8 @@ int tk_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* c_
 int tk_report_copy_out(tk_land* l, double f_opt, uint64_t* ranks, double* fitness,
                        double* fraction, double* pagerank) {
     if (int st = check_land(l)) return st;
-    if (!l->pr_done) return fail(TK_ESTATE, "report: run pagerank first");
+    if (!l->pr_done && !(l->sharded && l->shard_pr))
+        return fail(TK_ESTATE, "report: run pagerank first");
     const uint64_t m = l->n_minima;
     if (!m) return TK_OK;
     TKC(set_dev(l));

@@ -251,6 +251,60 @@ def test_virtual_gpu_shards_match_oracle(radix, nshards):
         s.land.close()
 
 
+def _gpu_ipc_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        radix = [8, 8, 6, 6, 4, 4, 2]
+        n = O.space_size(radix)
+        fit, ok = O.gen_iid(n, 0.2, 31)
+        shard = S.GpuShard(radix, rank, world, device=0)
+        shard.land.load_dense(fit, ok)
+        allreduce, allgather = S.torch_collectives()
+        S.connect_peers_ipc(shard, allgather)
+        res = S.analyze_sharded([shard], allreduce, allgather, O.ADJACENT)
+        r = shard.land.shard_pagerank_vector(shard.lo, shard.hi)
+        out.put((rank, res, shard.lo, r))
+        dist.barrier()  # peers stay mapped until everyone is done
+        shard.land.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_one_gpu_cuda_ipc():
+    """The multi-process path end to end on one device: two ranks, replicas
+    mapped with CUDA IPC, remote pushes through the mapped pointers."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        rk, res, lo, r = q.get(timeout=300)
+        got[rk] = (res, lo, r)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    radix = [8, 8, 6, 6, 4, 4, 2]
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, 0.2, 31)
+    ref = O.analyze(radix, fit, ok, O.ADJACENT, node_limit=1 << 32)
+    check(got[0][0], ref, fit, ok, O.ADJACENT)
+    r = np.concatenate([got[k][2] for k in (0, 1)])
+    assert np.abs(r - ref["pagerank"]).sum() <= 1e-12
+
+
 @pytest.mark.parametrize("kind", [O.ADJACENT, O.HAMMING])
 def test_two_process_gloo(kind):
     import torch.multiprocessing as mp
