@@ -49,10 +49,12 @@ _lib = None
 
 
 def load(path: str = LIB_PATH):
-    """Load libtk_landscape.so (building it first only if the toolchain is here)."""
+    """Load libtk_landscape.so (building it first only if the toolchain is here).
+    TK_LIB=<path> selects a build variant (paper_2210_01465_b200/build.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("TK_LIB", path)
     if not os.path.exists(path):
         from . import build as _b
         _b.build()

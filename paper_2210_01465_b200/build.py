@@ -48,23 +48,35 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+# experiment variants (A/B on the GPU via TK_LIB=<path>); "" is the product build
+VARIANTS = {
+    "": [],
+    "t256": ["-DTK_TILE=256", "-DTK_CTAS_PER_SM=2"],  # 256-rank tiles, two CTAs per SM
+}
+
+
+def lib_path(variant: str = "") -> str:
+    return LIB if not variant else LIB.replace(".so", f"_{variant}.so")
+
+
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    out = lib_path(variant)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "tk_landscape.h"))
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(out, deps):
+        return out
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *flags(["-Xptxas", "-v"] if verbose else []), "-c",
+        obj = os.path.join(CSRC, src.replace(".cu", f"{'_' + variant if variant else ''}.o"))
+        cmd = [nvcc(), *flags((["-Xptxas", "-v"] if verbose else []) + VARIANTS[variant]), "-c",
                os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    cmd = [nvcc(), *ARCH, "-ccbin", host_cxx(), "-shared", "-o", LIB, *objs]
+    cmd = [nvcc(), *ARCH, "-ccbin", host_cxx(), "-shared", "-o", out, *objs]
     subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var))

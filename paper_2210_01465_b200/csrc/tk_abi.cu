@@ -96,6 +96,7 @@ struct tk_land {
     int device = 0;
     int num_sms = 148;
     int smem_optin = 0;  // max dynamic shared memory per block
+    int smem_per_sm = 0;
     cudaStream_t stream = nullptr;
     std::vector<uint32_t> radix_in;
     std::vector<unsigned long long> strides_in;
@@ -143,6 +144,16 @@ struct tk_land {
 namespace {
 
 cudaError_t set_dev(const tk_land* l) { return cudaSetDevice(l->device); }
+
+// Shared memory the staged pipeline may use per block: TK_CTAS_PER_SM blocks
+// share an SM (1 by default; the 256-rank-tile build variant uses 2).
+#ifndef TK_CTAS_PER_SM
+#define TK_CTAS_PER_SM 1
+#endif
+int stage_budget(const tk_land* l) {
+    const int per = l->smem_per_sm / TK_CTAS_PER_SM - 2048;  // driver-reserved + static smem
+    return std::min(l->smem_optin, per) - 2048;
+}
 
 int check_land(const tk_land* l) {
     if (!l) return fail(TK_EINVAL, "null tk_land handle");
@@ -252,7 +263,7 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     TKC(cudaEventRecord(l->ev[0], l->stream));
     tk::StagePlan plan{};
     if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
-        tk::make_stage_plan(s, false, l->smem_optin - 4096, &plan)) {
+        tk::make_stage_plan(s, false, stage_budget(l), &plan)) {
         // T-rank tiles over the whole space, or over this handle's shard
         const uint64_t lo = l->sharded ? l->shard_lo : 0, hi = l->sharded ? l->shard_hi : n;
         const uint32_t nt = static_cast<uint32_t>((hi - lo + plan.T - 1) / plan.T);
@@ -400,7 +411,7 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     a.c1 = l->c1.as<double>();
     tk::StagePlan plan{};
     const bool have_plan = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
-                           tk::make_stage_plan(l->shape, true, l->smem_optin - 4096, &plan);
+                           tk::make_stage_plan(l->shape, true, stage_budget(l), &plan);
     l->pr_staged = have_plan;
     l->pr_done = false;
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
@@ -550,6 +561,7 @@ int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** o
     if (e == cudaSuccess) {
         l->num_sms = prop.multiProcessorCount;
         l->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+        l->smem_per_sm = static_cast<int>(prop.sharedMemPerMultiprocessor);
         if (!prop.cooperativeLaunch) e = cudaErrorNotSupported;
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking);
@@ -1044,7 +1056,7 @@ int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, do
     if (!l->shard_pr) return fail(TK_ESTATE, "shard step before tk_shard_pagerank_init");
     TKC(set_dev(l));
     tk::StagePlan plan{};
-    if (!tk::make_stage_plan(l->shape, true, l->smem_optin - 4096, &plan))
+    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan))
         return fail(TK_EINVAL, "shard step: no staging plan for this shape");
     Small* ds = l->small.as<Small>();
     tk::PrArgs a = shard_pr_args(l, damping);

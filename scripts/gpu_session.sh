@@ -32,6 +32,15 @@ if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   echo "exit=$?" >> "$OUT/bench_shard2.err"
 fi
 
+if [[ $WHAT == ab ]]; then
+  # A/B of build variants (paper_2210_01465_b200/build.py VARIANTS) on the bench workload
+  timeout 600 python bench.py --no-cpu --steps 5 > "$OUT/bench_base.json" 2> "$OUT/bench_base.err"
+  for v in ${VARIANTS:-t256}; do
+    TK_LIB=paper_2210_01465_b200/libtk_landscape_$v.so timeout 600 python bench.py --no-cpu \
+        --steps 5 > "$OUT/bench_$v.json" 2> "$OUT/bench_$v.err"
+  done
+fi
+
 if [[ $WHAT == all || $WHAT == ncu || $WHAT == quick ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu \
