@@ -52,6 +52,7 @@ def _stale(target: str, deps: list[str]) -> bool:
 VARIANTS = {
     "": [],
     "t256": ["-DTK_TILE=256", "-DTK_CTAS_PER_SM=2"],  # 256-rank tiles, two CTAs per SM
+    "split": ["-DTK_PR_SPLIT=1"],                     # 4 partial in-edge chains
 }
 
 

@@ -151,8 +151,9 @@ cudaError_t set_dev(const tk_land* l) { return cudaSetDevice(l->device); }
 #define TK_CTAS_PER_SM 1
 #endif
 int stage_budget(const tk_land* l) {
-    const int per = l->smem_per_sm / TK_CTAS_PER_SM - 2048;  // driver-reserved + static smem
-    return std::min(l->smem_optin, per) - 2048;
+    // per CTA: 1 KB driver reservation + static shared memory + margin
+    const int per = l->smem_per_sm / TK_CTAS_PER_SM - 3072;
+    return std::min(l->smem_optin - 2048, per);
 }
 
 int check_land(const tk_land* l) {
