@@ -59,3 +59,10 @@ if [[ $WHAT == all || $WHAT == ncu || $WHAT == quick ]]; then
   echo "exit=$?" >> "$OUT/ncu_pr.log"
 fi
 ls -la "$OUT"
+
+if [[ $WHAT == breakdown ]]; then
+  bash scripts/ncu_breakdown.sh "$TAG" pagerank c5
+  bash scripts/ncu_breakdown.sh "$TAG" ffg_count c5
+  TK_LIB=paper_2210_01465_b200/libtk_landscape_t256.so timeout 600 python bench.py --no-cpu \
+      --steps 5 > "$OUT/bench_t256.json" 2> "$OUT/bench_t256.err"
+fi
