@@ -81,6 +81,9 @@ int tk_device_count(int* count);
  * significant.  N = prod(radix) must be < 2^32 (u32 node ids, landscape.hpp:32). */
 int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** out);
 int tk_land_destroy(tk_land* land);
+/* Re-target a handle at another space shape, keeping its device buffers
+ * (they only grow): many small landscapes back to back without cudaMalloc. */
+int tk_land_reshape(tk_land* land, uint32_t dims, const uint32_t* radix);
 int tk_land_info(const tk_land* land, uint64_t* n_nodes, int* device);
 /* The cudaStream_t every kernel of this handle is launched on (for events). */
 void* tk_land_stream(tk_land* land);

@@ -21,7 +21,7 @@ TK_MAX_CP = 101
 # every symbol include/tk_landscape.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "tk_abi_version", "tk_last_error", "tk_status_name", "tk_device_count",
-    "tk_land_create", "tk_land_destroy", "tk_land_info", "tk_land_stream",
+    "tk_land_create", "tk_land_destroy", "tk_land_reshape", "tk_land_info", "tk_land_stream",
     "tk_land_kernel_info",
     "tk_land_load_dense", "tk_land_load_sparse", "tk_land_load_configs",
     "tk_land_generate", "tk_land_copy_fitness", "tk_land_lookup", "tk_optimum",
@@ -68,6 +68,7 @@ def load(path: str = LIB_PATH):
         "tk_device_count": (I, [C.POINTER(I)]),
         "tk_land_create": (I, [I, U32, P, C.POINTER(P)]),
         "tk_land_destroy": (I, [P]),
+        "tk_land_reshape": (I, [P, U32, P]),
         "tk_land_info": (I, [P, PU64, C.POINTER(I)]),
         "tk_land_stream": (P, [P]),
         "tk_land_kernel_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I),

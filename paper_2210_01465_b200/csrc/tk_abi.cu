@@ -578,6 +578,28 @@ int tk_land_create(int device, uint32_t dims, const uint32_t* radix, tk_land** o
     TK_GUARD_END
 }
 
+int tk_land_reshape(tk_land* l, uint32_t dims, const uint32_t* radix) {
+    if (int st = check_land(l)) return st;
+    if (dims == 0 || dims > TK_MAX_DIMS || !radix)
+        return fail(TK_EINVAL, "a space needs 1..32 parameters");
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < dims; ++i) {
+        if (radix[i] == 0) return fail(TK_EINVAL, "parameter with an empty value list");
+        n *= radix[i];
+        if (n > kMaxNodes)
+            return fail(TK_ELIMIT, "search space exceeds the u32 node-id range of the FFG");
+    }
+    if (l->sharded) return fail(TK_ESTATE, "reshape of a sharded handle");
+    l->radix_in.assign(radix, radix + dims);
+    l->strides_in.assign(dims, 1);
+    for (int i = static_cast<int>(dims) - 2; i >= 0; --i)
+        l->strides_in[i] = l->strides_in[i + 1] * radix[i + 1];
+    l->n = n;
+    l->loaded = l->built = l->emitted = l->pr_done = l->opt_ready = false;
+    l->hcap = 0;
+    return TK_OK;
+}
+
 int tk_land_destroy(tk_land* l) {
     if (!l) return TK_OK;
     cudaSetDevice(l->device);

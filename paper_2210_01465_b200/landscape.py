@@ -196,6 +196,16 @@ class Landscape:
         self.n_edges = 0
         self.n_minima = 0
 
+    def reshape(self, radix):
+        """Re-target this handle at another space, keeping its device buffers."""
+        r = np.ascontiguousarray(radix, np.uint32)
+        _check(self.L.tk_land_reshape(self.h, len(r), _ptr(r)))
+        self.radix = [int(x) for x in r]
+        n = C.c_uint64()
+        _check(self.L.tk_land_info(self.h, C.byref(n), None))
+        self.n = n.value
+        self.n_edges = self.n_minima = 0
+
     def close(self):
         if getattr(self, "h", None):
             self.L.tk_land_destroy(self.h)

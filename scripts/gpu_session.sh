@@ -66,3 +66,13 @@ if [[ $WHAT == breakdown ]]; then
   TK_LIB=paper_2210_01465_b200/libtk_landscape_t256.so timeout 600 python bench.py --no-cpu \
       --steps 5 > "$OUT/bench_t256.json" 2> "$OUT/bench_t256.err"
 fi
+
+if [[ $WHAT == probe ]]; then
+  # quick probes: staged-kernel residency of the variants, Hamming C5 bench line
+  for v in "" _t256; do
+    TK_DEBUG=1 TK_LIB=paper_2210_01465_b200/libtk_landscape$v.so timeout 300 python bench.py \
+        --no-cpu --steps 2 --workload c3 > "$OUT/probe$v.json" 2> "$OUT/probe$v.err"
+  done
+  timeout 900 python bench.py --no-cpu --steps 3 --kind hamming > "$OUT/bench_hamming.json" \
+      2> "$OUT/bench_hamming.err"
+fi
