@@ -46,7 +46,142 @@ WORKLOADS = {
                desc="synthetic 10-parameter space, 9,437,184 configs, heavy-tailed "
                     "runtimes G_heavy seed 3"),
 }
+WORKLOADS["c4"] = dict(desc="26 synthetic kernel spaces (4 paper shapes, PAPER.md:797-829, + 22 "
+                            "seeded shapes of 4-10 parameters, 864..82,944 configs) x 9 tables "
+                            "(seeds 0..8, generate_synthetic_kernel_space 'rugged'): 234 landscapes "
+                            "back to back")
 KIND = {"adjacent": 1, "hamming": 0}
+
+C4_PAPER = [("conv", (12, 6, 8, 8, 2, 2), 0.68), ("conv_mi50", (8, 6, 3, 3, 2), 0.52),
+            ("gemm", (4, 4, 3, 3, 3, 3, 4, 4, 2, 2), 0.78), ("pnpoly", (31, 11, 4, 2, 3), 0.04)]
+
+
+def c4_landscapes():
+    """26 shapes x 9 seeds; fail fractions per family."""
+    rng = np.random.default_rng(221001465)
+    shapes = list(C4_PAPER)
+    while len(shapes) < 26:
+        dims = int(rng.integers(4, 11))
+        radix = tuple(int(x) for x in rng.choice([2, 2, 3, 4, 4, 6, 8, 12, 16], size=dims))
+        if 864 <= int(np.prod(radix)) <= 82944:
+            shapes.append((f"s{len(shapes)}", radix, float(rng.uniform(0.0, 0.8))))
+    return [(name, radix, q, seed) for name, radix, q in shapes for seed in range(9)]
+
+
+def host_generator():
+    """libtunekit_b200.so's C export of generate_synthetic_kernel_space (the
+    C++ drop-in's host generator, bit-identical to the reference's)."""
+    import ctypes as C
+
+    path = os.path.join(ROOT, "cpp", "build", "libtunekit_b200.so")
+    if not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "cpp")], check=True)
+    L = C.CDLL(path)
+    L.tk_host_generate_synthetic.argtypes = [C.c_uint32, C.c_void_p, C.c_double, C.c_char_p,
+                                             C.c_uint64, C.c_void_p, C.c_void_p]
+
+    def gen(radix, q, seed):
+        r = np.asarray(radix, np.uint32)
+        n = int(np.prod(radix))
+        fit = np.empty(n, np.float64)
+        ok = np.empty(n, np.uint8)
+        st = L.tk_host_generate_synthetic(len(r), r.ctypes.data, q, b"rugged", seed,
+                                          fit.ctypes.data, ok.ctypes.data)
+        assert st == 0
+        return fit, ok
+    return gen
+
+
+def run_batch(args, wl, kind):
+    """C4: 234 small landscapes back to back through the C-ABI on one reused
+    handle (tk_land_reshape keeps the device buffers); with torchrun each rank
+    takes a balanced share (replicas, no collective) and time is the max over
+    ranks.  Every landscape: host upload, analyze_landscape, report read-back."""
+    import ctypes as C
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2210_01465_b200 as tk
+
+    items = sorted(c4_landscapes(), key=lambda x: -int(np.prod(x[1])))
+    mine = [it for i, it in enumerate(items) if i % world == rank]  # size-sorted round robin
+    gen = host_generator()
+    data = []
+    for name, radix, q, seed in mine:
+        fit, ok = gen(radix, q, seed)
+        fh = torch.empty(len(fit), dtype=torch.float64, pin_memory=True)
+        oh = torch.empty(len(fit), dtype=torch.uint8, pin_memory=True)
+        fh.numpy()[:] = fit
+        oh.numpy()[:] = ok
+        data.append((radix, fh, oh))
+    land = tk.Landscape(mine[0][1], device=local)
+    L = land.L
+    rep = [torch.empty(90000, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+
+    def one(radix, fh, oh):
+        land.reshape(radix)
+        assert L.tk_land_load_dense(land.h, C.c_void_p(fh.data_ptr()), C.c_void_p(oh.data_ptr()),
+                                    0) == 0, tk._abi.last_error()
+        s = land.analyze(kind, DAMPING, TOL, MAX_ITER, node_limit=1 << 32, p_max_percent=P_MAX)
+        assert L.tk_report_copy_out(land.h, s.f_opt, *[C.c_void_p(x.data_ptr()) for x in rep]) == 0
+        return s
+
+    def sweep():
+        return [one(*d) for d in data]
+
+    for _ in range(max(3, args.warmup)):
+        sweep()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(local)
+    t0 = time.perf_counter()
+    runs = [sweep() for _ in range(args.steps)]
+    torch.cuda.synchronize(local)
+    t_ms = (time.perf_counter() - t0) * 1e3
+    edges = sum(s.n_edges * (s.iterations + 1) for r in runs for s in r)
+    n_lands = len(items)
+    if dist is not None:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        e = torch.tensor([float(edges)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(e)
+        edges = float(e.item())
+    ms_step = t_ms / args.steps
+    pr_ms = float(np.mean([s.ms_pagerank for s in runs[-1]]))
+    if rank == 0:
+        print(json.dumps({
+            "metric": "FFG+PageRank GTEPS", "value": round(edges / (t_ms / 1e3) / 1e9, 3),
+            "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c4", "kind": args.kind, "desc": wl["desc"],
+                       "landscapes": n_lands, "parallelism": f"replicas{world}",
+                       "l2": "small landscapes; host upload per landscape inside the step"},
+            "s_per_space": round(ms_step / 1e3 / n_lands, 7),
+            "pagerank_kernel_ms_mean": round(pr_ms, 4),
+            "roofline": None,
+            "cpu_baseline": None,
+            "e2e": {"value": round(edges / (t_ms / 1e3) / 1e9, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": int(sum(9 * int(np.prod(it[1])) for it in items)),
+                    "d2h_bytes_per_step": int(sum(32 * s.n_minima for s in runs[-1]) * world),
+                    "note": "the step itself is end to end: host upload + report per landscape"},
+            "gpu_launches": int(n_lands * 9 * args.steps),
+        }))
+    land.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 KERNELS_PER_STEP = 6  # ffg_build, optimum x2, pagerank, cp_partial, cp_final
 DAMPING, TOL, MAX_ITER, P_MAX = 0.85, 1e-10, 100000, 15
 
@@ -464,7 +599,13 @@ def main() -> int:
     wl = WORKLOADS[args.workload]
     kind = KIND[args.kind]
     if args.impl == "reference":
+        if args.workload == "c4":
+            print(json.dumps({"impl": "reference", "unavailable": "the c4 reference arm is not "
+                              "implemented; use the default c5 workload"}))
+            return 0
         return run_reference(args, wl, kind)
+    if args.workload == "c4":
+        return run_batch(args, wl, kind)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         return run_sharded(args, wl, kind)
     return run_b200(args, wl, kind)

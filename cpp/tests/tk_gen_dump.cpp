@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "tunekit/cache_io.hpp"
 #include "tunekit/errors.hpp"
 #include "tunekit/generators.hpp"
 
@@ -49,6 +50,29 @@ int main(int argc, char** argv) {
             }
             std::fwrite(f.data(), 8, f.size(), stdout);
             std::fwrite(ok.data(), 1, ok.size(), stdout);
+            return 0;
+        }
+        if (mode == "loadcache") {  // tk_gen_dump loadcache <path> -> f64 fit, u8 ok, u8 present
+            SearchSpaceCache c = load_cache(argv[2]);
+            for (std::uint64_t r = 0; r < c.size(); ++r) {
+                const double v = c.mean(r);
+                std::fwrite(&v, 8, 1, stdout);
+            }
+            for (std::uint64_t r = 0; r < c.size(); ++r) {
+                const std::uint8_t o = c.present(r) && c.ok(r);
+                std::fwrite(&o, 1, 1, stdout);
+            }
+            for (std::uint64_t r = 0; r < c.size(); ++r) {
+                const std::uint8_t p = c.present(r);
+                std::fwrite(&p, 1, 1, stdout);
+            }
+            return 0;
+        }
+        if (mode == "savecache") {  // tk_gen_dump savecache <path> <q> <profile> <seed> <m0> ...
+            SearchSpaceCache c = generate_synthetic_kernel_space(
+                space_from(argc, argv, 6), std::atof(argv[3]), synthetic_profile(argv[4]),
+                std::strtoull(argv[5], nullptr, 10));
+            save_cache(c, argv[2]);
             return 0;
         }
         if (mode == "nk") {

@@ -15,4 +15,14 @@ CentralityReport analyze_landscape_limited(const SearchSpaceCache& cache, Neighb
                                            double damping, int p_max_percent,
                                            std::uint64_t node_limit);
 
+// analyze_landscape straight from a cache file (native or Kernel Tuner JSON,
+// cache_io.hpp): only the ok records travel to the GPU, as configuration
+// index vectors; the device encodes them to mixed-radix keys, builds an
+// open-addressing hash table of the valid set and densifies it (absent keys
+// become failed nodes).  No rank-indexed host table is built.  `space_out`
+// receives the parsed space (for report keys).
+CentralityReport analyze_cache_file(const std::string& path, NeighbourhoodKind kind,
+                                    double damping, int p_max_percent, std::uint64_t node_limit,
+                                    ParameterSpace* space_out = nullptr);
+
 }  // namespace tunekit

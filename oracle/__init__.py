@@ -94,6 +94,10 @@ def ref():
         R.ref_generate_nk.argtypes = [C.c_int, C.c_int, C.c_uint64, _f64p]
         R.ref_optimum.argtypes = [C.c_uint32, _u32p, _f64p, _u8p, C.POINTER(C.c_double),
                                   C.POINTER(C.c_uint64)]
+        R.ref_load_cache.restype = C.c_longlong
+        R.ref_load_cache.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        R.ref_save_synthetic.argtypes = [C.c_uint32, _u32p, C.c_double, C.c_char_p, C.c_uint64,
+                                         C.c_char_p]
         R.ref_ffg.argtypes = [C.c_uint32, _u32p, _f64p, _u8p, C.c_int, _u64p, _u32p,
                               C.c_uint64, _u8p, _u32p, C.POINTER(C.c_uint64),
                               C.POINTER(C.c_uint64)]

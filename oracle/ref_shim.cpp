@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "tunekit/cache.hpp"
+#include "tunekit/cache_io.hpp"
 #include "tunekit/errors.hpp"
 #include "tunekit/generators.hpp"
 #include "tunekit/space.hpp"
@@ -151,6 +152,37 @@ int ref_ffg(std::uint32_t dims, const std::uint32_t* radix, const double* fit,
     *n_edges = e;
     *n_minima = m;
     return 0;
+}
+
+// load_cache (cache_io.cpp:114-124) -> size, means, ok, present flags.
+// Call with fit == nullptr to query the size; returns -1 on a parse error.
+long long ref_load_cache(const char* path, double* fit, std::uint8_t* ok, std::uint8_t* present) {
+    try {
+        SearchSpaceCache c = load_cache(path);
+        if (fit) {
+            for (std::uint64_t r = 0; r < c.size(); ++r) {
+                fit[r] = c.mean(r);
+                ok[r] = c.present(r) && c.ok(r);
+                present[r] = c.present(r);
+            }
+        }
+        return static_cast<long long>(c.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// save_cache of generate_synthetic_kernel_space (cache_io.cpp:126-160)
+int ref_save_synthetic(std::uint32_t dims, const std::uint32_t* radix, double q,
+                       const char* profile, std::uint64_t seed, const char* path) {
+    try {
+        save_cache(generate_synthetic_kernel_space(make_space(dims, radix), q,
+                                                   synthetic_profile(profile), seed),
+                   path);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
 }
 
 }  // extern "C"

@@ -128,6 +128,44 @@ def main() -> None:
         if nn <= 12:
             arrays[key + "_fit"] = fit
 
+    # cache files: one written by the reference's save_cache, one Kernel Tuner
+    # style file (tune_params, error strings, null, times arrays, booleans);
+    # the expected tables are the reference's own load_cache of each
+    native = os.path.join(HERE, "cache_native.json")
+    assert R.ref_save_synthetic(3, np.array([3, 4, 2], np.uint32), 0.25, b"rugged", 5,
+                                native.encode()) == 0
+    kt = {"kernel_name": "kt_demo", "device_name": "B200",
+          "tune_params_keys": ["block", "tile", "unroll"],
+          "tune_params": {"block": [128, 32, 64], "tile": [1, 2], "unroll": [True, False]},
+          "cache": {}}
+    rng = np.random.default_rng(11)
+    for b in (32, 64, 128):
+        for t in (1, 2):
+            for u in (0, 1):
+                key = f"{b},{t},{u}"
+                r = rng.random()
+                if r < 0.2:
+                    kt["cache"][key] = {"time": "CompilationFailedConfig"}
+                elif r < 0.3:
+                    kt["cache"][key] = None
+                elif r < 0.6:
+                    kt["cache"][key] = {"times": [float(x) for x in rng.random(4) + 1.0]}
+                else:
+                    kt["cache"][key] = {"time": float(rng.random() + 1.0)}
+    ktp = os.path.join(HERE, "cache_kt.json")
+    with open(ktp, "w") as f:
+        json.dump(kt, f, indent=1)
+    meta["cache_files"] = []
+    for name, path in (("cache_native", native), ("cache_kt", ktp)):
+        n = R.ref_load_cache(path.encode(), None, None, None)
+        assert n > 0
+        fit = np.empty(n, np.float64)
+        ok = np.empty(n, np.uint8)
+        pres = np.empty(n, np.uint8)
+        assert R.ref_load_cache(path.encode(), fit.ctypes.data, ok.ctypes.data, pres.ctypes.data) == n
+        arrays[name + "_fit"], arrays[name + "_ok"], arrays[name + "_present"] = fit, ok, pres
+        meta["cache_files"].append(dict(name=name, file=os.path.basename(path), size=int(n)))
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)

@@ -128,3 +128,66 @@ def test_dropin_on_gpu_matches_oracle(built, tmp_path, exe):
         lines = open(os.path.join(tmp_path, f"minima_{name}.csv")).read().splitlines()
         assert lines[0].startswith("rank,") and len(lines) == len(g["minima"]) + 1
     assert open(os.path.join(tmp_path, "graph.dot")).read().startswith("digraph")
+
+
+# ----------------------------------------------------------- cache files --
+
+def test_load_cache_matches_reference(built, golden):
+    """cache_io.cpp against the reference's own load_cache of the same files
+    (a reference-written native cache and a Kernel Tuner style file)."""
+    meta, arrays = golden
+    gd = os.path.join(ROOT, "tests", "golden")
+    for rec in meta["cache_files"]:
+        out = dump(built, "loadcache", os.path.join(gd, rec["file"]))
+        n = rec["size"]
+        fit = np.frombuffer(out[: 8 * n], np.float64)
+        ok = np.frombuffer(out[8 * n: 9 * n], np.uint8)
+        pres = np.frombuffer(out[9 * n:], np.uint8)
+        assert np.array_equal(fit.view(np.uint64), arrays[rec["name"] + "_fit"].view(np.uint64))
+        assert np.array_equal(ok, arrays[rec["name"] + "_ok"])
+        assert np.array_equal(pres, arrays[rec["name"] + "_present"])
+
+
+def test_save_load_round_trip(built, tmp_path):
+    path = str(tmp_path / "c.json")
+    dump(built, "savecache", path, 0.3, "rugged", 9, 5, 4, 3)
+    out = dump(built, "loadcache", path)
+    n = 60
+    fit = np.frombuffer(out[: 8 * n], np.float64)
+    ok = np.frombuffer(out[8 * n: 9 * n], np.uint8)
+    ref_fit, ref_ok = O.gen_synthetic([5, 4, 3], 0.3, "rugged", 9)
+    assert np.array_equal(fit.view(np.uint64), ref_fit.view(np.uint64))
+    assert np.array_equal(ok, ref_ok)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ingest", [[], ["--device-ingest"]])
+def test_analyze_cli_matches_oracle(built, tmp_path, ingest):
+    import json
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    radix, q, seed = [8, 6, 3, 3, 2], 0.52, 3
+    path = str(tmp_path / "cache.json")
+    dump(built, "savecache", path, q, "rugged", seed, *radix)
+    rep_path = str(tmp_path / "rep.json")
+    r = subprocess.run([os.path.join(built, "tk_analyze"), path, "--json", rep_path,
+                        "--minima-csv", str(tmp_path / "m.csv"), *ingest],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rep = json.load(open(rep_path))
+    fit, ok = O.gen_synthetic(radix, q, "rugged", seed)
+    ref = O.analyze(radix, fit, ok, O.ADJACENT)
+    assert rep["pagerank_iterations"] == ref["iterations"]
+    assert [m["rank"] for m in rep["minima"]] == [int(x) for x in ref["ffg"]["minima"]]
+    for e, (k, c) in zip(rep["c_p_curve"], ref["c_p_curve"]):
+        assert e["p_percent"] == k and abs(e["c_p"] - c) <= 1e-9
+    # exit codes of errors.hpp:8-9
+    bad = subprocess.run([os.path.join(built, "tk_analyze"), path, "--neighbourhood", "diagonal"],
+                         capture_output=True, text=True)
+    assert bad.returncode == 2
+    missing = subprocess.run([os.path.join(built, "tk_analyze"), str(tmp_path / "none.json")],
+                             capture_output=True, text=True)
+    assert missing.returncode == 1
