@@ -53,6 +53,9 @@ VARIANTS = {
     "": [],
     "t256": ["-DTK_TILE=256", "-DTK_CTAS_PER_SM=2"],  # 256-rank tiles, two CTAs per SM
     "split": ["-DTK_PR_SPLIT=1"],                     # 4 partial in-edge chains
+    "p1": ["-DTK_PROD_WARPS=1"],                      # one producer warp (round-1 layout)
+    "p2": ["-DTK_PROD_WARPS=2"],
+    "ev": ["-DTK_EVICT=1"],                           # L2 evict-first on streamed data
 }
 
 
