@@ -55,7 +55,7 @@ VARIANTS = {
     "split": ["-DTK_PR_SPLIT=1"],                     # 4 partial in-edge chains
     "p1": ["-DTK_PROD_WARPS=1"],                      # one producer warp (round-1 layout)
     "p2": ["-DTK_PROD_WARPS=2"],
-    "ev": ["-DTK_EVICT=1"],                           # L2 evict-first on streamed data
+    "ne": ["-DTK_NO_EVICT=1"],                        # no L2 evict-first hints
 }
 
 

@@ -150,6 +150,7 @@ struct StagePlan {
     int far_len;           // elements per far range (even)
     int aux_bytes;         // bytes before the f64 region (pw + r for PageRank, ok for FFG)
     int stage_bytes;
+    unsigned int far_ef;   // far ranges whose L2 lines are loaded evict-first (bit f)
     unsigned long long npad2;  // f64 arrays hold at least this many elements (even)
     unsigned long long npad16; // u8/u32 arrays are padded to this many elements
 };
