@@ -52,7 +52,6 @@ def _stale(target: str, deps: list[str]) -> bool:
 VARIANTS = {
     "": [],
     "t256": ["-DTK_TILE=256", "-DTK_CTAS_PER_SM=2"],  # 256-rank tiles, two CTAs per SM
-    "split": ["-DTK_PR_SPLIT=1"],                     # 4 partial in-edge chains
     "p1": ["-DTK_PROD_WARPS=1"],                      # one producer warp (round-1 layout)
     "p2": ["-DTK_PROD_WARPS=2"],
     "ne": ["-DTK_NO_EVICT=1"],                        # no L2 evict-first hints

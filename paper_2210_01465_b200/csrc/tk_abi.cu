@@ -412,7 +412,7 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     a.c1 = l->c1.as<double>();
     tk::StagePlan plan{};
     const bool have_plan = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
-                           tk::make_stage_plan(l->shape, true, stage_budget(l), &plan);
+                           tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false);
     l->pr_staged = have_plan;
     l->pr_done = false;
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,

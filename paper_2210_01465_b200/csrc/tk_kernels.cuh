@@ -146,6 +146,9 @@ struct StagePlan {
     int lo_src[kMaxDims];  // f64 smem index (plus t) of the lower neighbour of dim i
     int hi_src[kMaxDims];  // ... upper neighbour
     int own_src;           // ... of the node itself
+    int lo_off[kMaxDims];  // the same as byte offsets (8 * src)
+    int hi_off[kMaxDims];
+    int own_off;
     int near_len;          // elements in the near window (even)
     int far_len;           // elements per far range (even)
     int aux_bytes;         // bytes before the f64 region (pw + r for PageRank, ok for FFG)
@@ -155,7 +158,10 @@ struct StagePlan {
     unsigned long long npad16; // u8/u32 arrays are padded to this many elements
 };
 // kind_pr: PageRank layout (u32 pw[T], f64 r[T], window) vs FFG (u8 ok[T], window)
-bool make_stage_plan(const DevShape& s, bool kind_pr, int smem_budget, StagePlan* plan);
+// stage_r: PageRank stages the old ranks too (the sharded step); the single-GPU
+// kernel stores contributions only and stages pw + window
+bool make_stage_plan(const DevShape& s, bool kind_pr, int smem_budget, StagePlan* plan,
+                     bool stage_r = true);
 // count (staged) -> tile scans -> fill; a.e_status/m_status/tile_counter are the
 // scan scratch (>= ceil(ntiles/256) tiles), totals[0..1] are written by the scan.
 cudaError_t launch_ffg_build_staged(const DevShape& s, const StagePlan& p, bool emit,
