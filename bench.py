@@ -400,8 +400,11 @@ def run_b200(args, wl, kind):
     n = land.n
     it_last = sums[-1].iterations
     if land_mode_packed(radix, kind):
-        per_iter, per_pro = 36 * n, 20 * n
-        model = "36 B/node/iteration: packed word 4 + r_old 8 + r_new 8 + c_new 8 + c gather 8"
+        # contribution-only iteration: packed word 4 + c read once 8 + c' 8;
+        # prologue writes c_0 (pw 4 + 8), the closing pass materialises r' (pw 4 + c 8 + r 8)
+        per_iter, per_pro = 20 * n, 12 * n + 20 * n
+        model = ("20 B/node/iteration: packed word 4 + c gather (each c read once) 8 + c' 8; "
+                 "+ 12 B/node prologue (c_0) + 20 B/node closing r' pass")
     else:
         per_iter, per_pro = 37 * n, 21 * n
         model = "37 B/node/iteration: mask 4 + outdeg 1 + r_old 8 + r_new 8 + c_new 8 + c 8"
