@@ -55,6 +55,8 @@ VARIANTS = {
     "p1": ["-DTK_PROD_WARPS=1"],                      # one producer warp (round-1 layout)
     "p2": ["-DTK_PROD_WARPS=2"],
     "ne": ["-DTK_NO_EVICT=1"],                        # no L2 evict-first hints
+    "trace": ["-DTK_TRACE=1"],                        # per-tile timeline of block 0 (stderr)
+    "p6": ["-DTK_PROD_WARPS=6"],
 }
 
 
