@@ -57,6 +57,10 @@ VARIANTS = {
     "ne": ["-DTK_NO_EVICT=1"],                        # no L2 evict-first hints
     "trace": ["-DTK_TRACE=1"],                        # per-tile timeline of block 0 (stderr)
     "p6": ["-DTK_PROD_WARPS=6"],
+    # timing experiments (wrong results, fixed 29 iterations)
+    "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],
+    "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
+    "xnocomp0": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1", "-DTK_X_NODIM0=1"],
 }
 
 

@@ -186,7 +186,7 @@ __global__ void tma_pipes(const uint8_t* __restrict__ src, size_t nbytes, int st
 
 // P producer warps (stage k issued by warp k % P), C consumer warps, one pipeline
 __global__ void tma_mp(const uint8_t* __restrict__ src, size_t nbytes, int stage_bytes, int S,
-                       int ncopy, int P, int C, unsigned long long* sink) {
+                       int ncopy, int P, int C, unsigned long long* sink, int passes = 1) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[32], empty[32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -198,18 +198,22 @@ __global__ void tma_mp(const uint8_t* __restrict__ src, size_t nbytes, int stage
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    const size_t ntiles = nbytes / stage_bytes;
+    const size_t nt1 = nbytes / stage_bytes;
+    const size_t ntiles = nt1 * passes;
     const uint32_t cb = stage_bytes / ncopy;
     if (w < P) {
         uint32_t k = w;
-        for (size_t j = blockIdx.x + (size_t)w * gridDim.x; j < ntiles; j += (size_t)gridDim.x * P, k += P) {
+        size_t jm = blockIdx.x + (size_t)w * gridDim.x;
+        for (size_t j = jm; j < ntiles; j += (size_t)gridDim.x * P, k += P) {
             const int st = k % S;
             if (k >= (uint32_t)S) mbar_wait(&empty[st], ((k / S) - 1) & 1u);
-            if (lane == 0) mbar_expect_tx(&full[st], stage_bytes);
+            while (jm >= nt1) jm -= nt1;
+            if (lane == 0) mbar_expect_tx(&full[st], (stage_bytes / ncopy) * ncopy);
             __syncwarp();
             for (int c = lane; c < ncopy; c += 32)
-                bulk(smem + (size_t)st * stage_bytes + c * cb, src + j * stage_bytes + (size_t)c * cb, cb,
+                bulk(smem + (size_t)st * stage_bytes + c * cb, src + jm * stage_bytes + (size_t)c * cb, cb,
                      &full[st], 0, false);
+            jm += (size_t)gridDim.x * P;
         }
     } else {
         uint32_t k = 0;
@@ -301,6 +305,31 @@ int main(int argc, char** argv) {
                     bytes / ms / 1e6);
     };
     const int mode = argc > 1 ? std::atoi(argv[1]) : 0;
+    if (mode == 4) {
+        CK(cudaFuncSetAttribute(tma_mp, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        for (size_t buf_mb : {32, 96, 4096})
+            for (int S : {3, 4})
+                for (int nc : {2, 4, 7, 14, 28}) {
+                    const int stage = 57344 / (nc * 16) * 16 * nc;
+                    const int P = 2, C = 16;
+                    const size_t nb = buf_mb << 20;
+                    const int passes = (int)((4096ull << 20) / nb);
+                    const size_t smem = (size_t)stage * S;
+                    tma_mp<<<sms, 32 * (P + C), smem>>>(buf, nb, stage, S, nc, P, C, sink, 1);
+                    CK(cudaGetLastError());
+                    CK(cudaEventRecord(e0));
+                    tma_mp<<<sms, 32 * (P + C), smem>>>(buf, nb, stage, S, nc, P, C, sink, passes);
+                    CK(cudaEventRecord(e1));
+                    CK(cudaEventSynchronize(e1));
+                    float ms;
+                    CK(cudaEventElapsedTime(&ms, e0, e1));
+                    const double bytes = (double)(nb / stage) * stage * passes;
+                    std::printf("mp4 buf=%5zuMB S=%d stage=%6d copies=%2d (%5d B) : %8.1f GB/s  %.1f B/clk/SM\n",
+                                buf_mb, S, stage, nc, stage / nc, bytes / ms / 1e6,
+                                bytes / ms / 1e6 / sms / 1.92);
+                }
+        return 0;
+    }
     if (mode == 3) {
         CK(cudaFuncSetAttribute(tma_mp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         for (int C : {1, 16})
