@@ -391,6 +391,20 @@ class Landscape:
         _check(self.L.tk_shard_pagerank_copy_out(self.h, _ptr(r)))
         return r
 
+    def load_dense_host_ptrs(self, fitness_ptr: int, ok_ptr: int):
+        """Upload from host buffers given as raw pointers (pinned memory for
+        asynchronous DMA); one entry per configuration."""
+        _check(self.L.tk_land_load_dense(self.h, C.c_void_p(fitness_ptr), C.c_void_p(ok_ptr),
+                                         _abi.TK_MEM_HOST))
+
+    def report_copy_out_ptrs(self, f_opt: float, rank_ptr: int, fit_ptr: int, ratio_ptr: int,
+                             pr_ptr: int):
+        """Minima report rows (rank u32 as u64 slot, fitness, f_opt/f, PageRank) into
+        caller buffers of n_minima entries each (host or pinned)."""
+        _check(self.L.tk_report_copy_out(self.h, f_opt, C.c_void_p(rank_ptr),
+                                         C.c_void_p(fit_ptr), C.c_void_p(ratio_ptr),
+                                         C.c_void_p(pr_ptr)))
+
     def analyze(self, kind: int, damping=0.85, tol=1e-10, max_iter=100000,
                 node_limit=1_000_000, p_max_percent=15, emit_csr=False):
         s = _abi.ReportSummary()
@@ -400,6 +414,67 @@ class Landscape:
         self.kind = kind
         self.n_edges, self.n_minima = s.n_edges, s.n_minima
         return s
+
+
+class AnalysisPipeline:
+    """End-to-end analysis of a stream of search spaces of one shape, double
+    buffered over two device handles: while one handle runs analyze_landscape,
+    a worker thread reads the previous space's minima report back from the
+    other handle and uploads the next space's table into it (its own CUDA
+    stream, DMA from pinned host memory), so the PCIe transfers of step k+1
+    overlap the kernels of step k.  Every step still moves its whole input
+    table host->device and its report device->host.
+
+    items: sequence of (fitness_ptr, ok_ptr) pinned host buffers (ints);
+    reports: per step a tuple of four pointers (rank, fitness, ratio, pagerank)
+    with room for n_minima entries, or None to skip the read-back.
+    """
+
+    def __init__(self, radix, device: int = 0):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.lands = [Landscape(radix, device), Landscape(radix, device)]
+        self.pool = ThreadPoolExecutor(1)
+
+    def close(self):
+        self.pool.shutdown(wait=True)
+        for land in self.lands:
+            land.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def run(self, items, kind: int, reports=None, **analyze_kw):
+        """Analyse every item; returns the list of report summaries.  The
+        worker queue is FIFO: upload(k), read_back(k - 1), upload(k + 1), ...
+        so a handle's read-back always precedes its next upload, and the main
+        thread waits for upload(k) before analysing on handle k % 2."""
+        n = len(items)
+        out = [None] * n
+        if n == 0:
+            return out
+
+        def upload(k):
+            self.lands[k % 2].load_dense_host_ptrs(*items[k])
+
+        def read_back(k, s):
+            if reports is not None and reports[k] is not None:
+                self.lands[k % 2].report_copy_out_ptrs(s.f_opt, *reports[k])
+
+        fut_up = self.pool.submit(upload, 0)
+        pending = []
+        for k in range(n):
+            fut_up.result()  # table k resident on handle k % 2
+            if k + 1 < n:
+                fut_up = self.pool.submit(upload, k + 1)  # overlaps analyze(k)
+            out[k] = self.lands[k % 2].analyze(kind, **analyze_kw)
+            pending.append(self.pool.submit(read_back, k, out[k]))  # overlaps analyze(k + 1)
+        for f in pending:
+            f.result()
+        return out
 
 
 # ------------------------------------------------- reference-shaped calls --

@@ -320,3 +320,32 @@ def test_c3_scale_properties_and_parity(tk, radix, kind, gen, q):
     assert np.all(np.diff(cps) >= -1e-15) and 0 <= cps[0] and cps[-1] <= 1 + 1e-15
     rr, rit, _ = O.pagerank(off, tg, nthreads=8)
     assert it == rit and rel_l1(r, rr) <= PR_RTOL
+
+
+def test_analysis_pipeline_matches_single_handle(tk):
+    """tk.AnalysisPipeline (double-buffered uploads / report read-backs over two
+    handles) returns, per space, exactly what one handle's analyze + report
+    rows return, on a stream of different spaces of one shape."""
+    radix = [8, 6, 6, 4, 4, 2]
+    tables = [O.gen_synthetic(radix, q, "rugged", seed) for seed, q in
+              ((0, 0.3), (1, 0.1), (2, 0.5), (3, 0.0), (4, 0.2))]
+    want = []
+    for fit, ok in tables:
+        with tk.Landscape(radix) as land:
+            land.load_dense(fit, ok)
+            s = land.analyze(tk.ADJACENT, emit_csr=True)
+            want.append((s.iterations, s.n_edges, s.n_minima, list(s.c_p[:16]),
+                         land.report_rows(s.f_opt)))
+    hosts = [(np.ascontiguousarray(f, np.float64), np.ascontiguousarray(o, np.uint8))
+             for f, o in tables]
+    items = [(f.ctypes.data, o.ctypes.data) for f, o in hosts]
+    bufs = [[np.empty(max(1, w[2]), dt) for dt in (np.uint64, np.float64, np.float64,
+                                                   np.float64)] for w in want]
+    reports = [tuple(b.ctypes.data for b in bb) for bb in bufs]
+    with tk.AnalysisPipeline(radix) as pipe:
+        got = pipe.run(items, tk.ADJACENT, reports, emit_csr=True)
+    for s, w, bb in zip(got, want, bufs):
+        assert (s.iterations, s.n_edges, s.n_minima) == w[:3]
+        assert list(s.c_p[:16]) == w[3]
+        for a, b in zip(bb, w[4]):
+            assert np.array_equal(a[: w[2]], b)
