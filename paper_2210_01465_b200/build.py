@@ -61,6 +61,7 @@ VARIANTS = {
     "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],
     "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
     "xnocomp0": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1", "-DTK_X_NODIM0=1"],
+    "xhalf": ["-DTK_X_ITERS=29", "-DTK_X_HALFLDS=1"],
 }
 
 
