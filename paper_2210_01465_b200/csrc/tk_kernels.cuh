@@ -154,6 +154,14 @@ struct StagePlan {
     int aux_bytes;         // bytes before the f64 region (pw + r for PageRank, ok for FFG)
     int stage_bytes;
     unsigned int far_ef;   // far ranges whose L2 lines are loaded evict-first (bit f)
+    // FFG count digit classes (bit i = dim i), tile T at rank v0, P_i = s_i * m_i:
+    //   dim_inv:  P_i divides T -> x_i = (t mod P_i) / s_i, fixed per thread
+    //   dim_uni:  T divides s_i -> x_i constant over the tile; its border bits
+    //             are staged per tile in the stage header
+    //   dim_tile: T divides P_i otherwise -> x_i = ((v0 mod P_i) + t) / s_i with
+    //             v0 mod P_i staged in the header
+    //   the rest: decoded per rank from the rank
+    unsigned int dim_inv, dim_uni, dim_tile;
     unsigned long long npad2;  // f64 arrays hold at least this many elements (even)
     unsigned long long npad16; // u8/u32 arrays are padded to this many elements
 };
