@@ -186,6 +186,20 @@ KERNELS_PER_STEP = 6  # ffg_build, optimum x2, pagerank, cp_partial, cp_final
 DAMPING, TOL, MAX_ITER, P_MAX = 0.85, 1e-10, 100000, 15
 
 
+def measured_traffic(workload: str, kind: str, iterations: int):
+    """DRAM bytes (read + write) per PageRank launch from the committed ncu
+    --set full capture (profiles/r01_pagerank_traffic.json), when it was taken
+    on this workload; None otherwise."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_pagerank_traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if (t.get("workload"), t.get("kind"), t.get("iterations")) != (workload, kind, iterations):
+        return None
+    return t["dram_bytes_per_launch"]
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -413,7 +427,8 @@ def run_b200(args, wl, kind):
     ffg_ms = float(np.mean([x.ms_ffg for x in sums]))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                "traffic": None, "kernel": "pagerank_kernel (persistent, cooperative)",
+                "traffic": measured_traffic(args.workload, args.kind, it_last),
+                "kernel": "pagerank_staged_kernel (persistent, cooperative)",
                 "bytes_model": model, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pr_bytes, "kernel_ms": round(pr_ms, 3),
                 "iterations": it_last, "kernels": kinfo}

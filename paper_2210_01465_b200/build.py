@@ -57,6 +57,8 @@ VARIANTS = {
     "ne": ["-DTK_NO_EVICT=1"],                        # no L2 evict-first hints
     "trace": ["-DTK_TRACE=1"],                        # per-tile timeline of block 0 (stderr)
     "p6": ["-DTK_PROD_WARPS=6"],
+    "pw3": ["-DTK_PW_AHEAD=3"],
+    "pw4": ["-DTK_PW_AHEAD=4"],
     # timing experiments (wrong results, fixed 29 iterations)
     "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],
     "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
