@@ -123,20 +123,18 @@ def run_batch(args, wl, kind):
         fh.numpy()[:] = fit
         oh.numpy()[:] = ok
         data.append((radix, fh, oh))
-    land = tk.Landscape(mine[0][1], device=local)
-    L = land.L
-    rep = [torch.empty(90000, dtype=torch.float64, pin_memory=True) for _ in range(4)]
-
-    def one(radix, fh, oh):
-        land.reshape(radix)
-        assert L.tk_land_load_dense(land.h, C.c_void_p(fh.data_ptr()), C.c_void_p(oh.data_ptr()),
-                                    0) == 0, tk._abi.last_error()
-        s = land.analyze(kind, DAMPING, TOL, MAX_ITER, node_limit=1 << 32, p_max_percent=P_MAX)
-        assert L.tk_report_copy_out(land.h, s.f_opt, *[C.c_void_p(x.data_ptr()) for x in rep]) == 0
-        return s
+    workers = int(os.environ.get("TK_BATCH_WORKERS", "8"))
+    batch = tk.BatchAnalyzer(device=local, workers=workers, radix0=mine[0][1])
+    items = [(radix, fh.data_ptr(), oh.data_ptr()) for radix, fh, oh in data]
+    reps = [[torch.empty(90000, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+            for _ in range(workers)]
+    # one report buffer set per worker slot is enough for timing; item k uses set k % workers
+    reports = [tuple(t.data_ptr() for t in reps[k % workers]) for k in range(len(items))]
+    akw = dict(damping=DAMPING, tol=TOL, max_iter=MAX_ITER, node_limit=1 << 32,
+               p_max_percent=P_MAX)
 
     def sweep():
-        return [one(*d) for d in data]
+        return batch.run(items, kind, reports, **akw)
 
     for _ in range(max(3, args.warmup)):
         sweep()
@@ -166,6 +164,7 @@ def run_batch(args, wl, kind):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c4", "kind": args.kind, "desc": wl["desc"],
                        "landscapes": n_lands, "parallelism": f"replicas{world}",
+                       "host_workers": workers,
                        "l2": "small landscapes; host upload per landscape inside the step"},
             "s_per_space": round(ms_step / 1e3 / n_lands, 7),
             "pagerank_kernel_ms_mean": round(pr_ms, 4),
@@ -174,10 +173,11 @@ def run_batch(args, wl, kind):
             "e2e": {"value": round(edges / (t_ms / 1e3) / 1e9, 3), "unit": "GTEPS",
                     "h2d_bytes_per_step": int(sum(9 * int(np.prod(it[1])) for it in items)),
                     "d2h_bytes_per_step": int(sum(32 * s.n_minima for s in runs[-1]) * world),
-                    "note": "the step itself is end to end: host upload + report per landscape"},
+                    "note": "the step itself is end to end: host upload + report per landscape "
+                            "(tk.BatchAnalyzer: concurrent handles/streams)"},
             "gpu_launches": int(n_lands * 9 * args.steps),
         }))
-    land.close()
+    batch.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -7,7 +7,7 @@ script (`build`).  Importing it does not touch the GPU.
 """
 from . import _abi  # noqa: F401
 from .landscape import (  # noqa: F401
-    ADJACENT, HAMMING, AnalysisPipeline, CentralityReport, Error, FitnessFlowGraph, InvalidArgument,
+    ADJACENT, HAMMING, AnalysisPipeline, BatchAnalyzer, CentralityReport, Error, FitnessFlowGraph, InvalidArgument,
     Landscape, MinimaFractionReport, NoFeasiblePoint, NonConvergence, PointCensus,
     SearchSpaceCache, analyze_landscape, build_ffg, classify_points,
     minima_fraction_report, neighbourhood_from_string, pagerank, proportion_of_centrality)

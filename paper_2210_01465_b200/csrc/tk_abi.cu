@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -357,12 +358,72 @@ int nonconv(long long it, double res) {
 }
 
 // Runs the persistent PageRank kernel over buffers already described by `a`.
+// Cooperative (grid-synchronising) PageRank launches from different streams
+// (tk.BatchAnalyzer drives several handles at once) may run concurrently only
+// while their SM footprints sum to at most the device's SM count: two
+// persistent cooperative grids that each hold part of the SMs the other needs
+// would spin in grid.sync forever.  Per device, the in-flight cooperative
+// launches are tracked as (completion event, SMs); a launch that does not fit
+// makes its stream wait for the oldest ones first.  Non-cooperative kernels
+// always finish, so they cannot close such a cycle.
+struct CoopGate {
+    std::mutex mu;
+    struct Flight {
+        cudaEvent_t ev;
+        int sms;
+    };
+    std::vector<Flight> inflight[64];
+    std::vector<cudaEvent_t> spare;
+};
+CoopGate& coop_gate() {
+    static CoopGate g;
+    return g;
+}
+template <class F>
+cudaError_t gated_coop_launch(int device, int num_sms, int footprint_sms, cudaStream_t stream,
+                              F&& launch) {
+    CoopGate& g = coop_gate();
+    std::lock_guard<std::mutex> lk(g.mu);
+    auto& fl = g.inflight[device & 63];
+    int used = 0;
+    for (size_t i = 0; i < fl.size();) {  // drop completed launches
+        if (cudaEventQuery(fl[i].ev) == cudaSuccess) {
+            g.spare.push_back(fl[i].ev);
+            fl.erase(fl.begin() + static_cast<long>(i));
+        } else {
+            used += fl[i].sms;
+            ++i;
+        }
+    }
+    (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+    const int need = std::min(footprint_sms, num_sms);
+    while (!fl.empty() && used + need > num_sms) {  // wait for the oldest
+        cudaError_t e = cudaStreamWaitEvent(stream, fl.front().ev, 0);
+        if (e != cudaSuccess) return e;
+        used -= fl.front().sms;
+        g.spare.push_back(fl.front().ev);
+        fl.erase(fl.begin());
+    }
+    cudaError_t e = launch();
+    if (e != cudaSuccess) return e;
+    cudaEvent_t ev;
+    if (!g.spare.empty()) {
+        ev = g.spare.back();
+        g.spare.pop_back();
+    } else if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+        return e;
+    }
+    e = cudaEventRecord(ev, stream);
+    if (e != cudaSuccess) return e;
+    fl.push_back({ev, need});
+    return cudaSuccess;
+}
+
 int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool wide,
                  tk::PrArgs a, DevBuf& part, Small* ds, Small* hs, cudaStream_t stream,
                  double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
                  cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr,
                  const tk::StagePlan* plan = nullptr) {
-    (void)device;
     const int maxg = plan ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
     TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
@@ -381,8 +442,15 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
     a.out_status = &ds->pr.status;
     int g = 0;
     if (e0) TKC(cudaEventRecord(e0, stream));
-    if (plan) TKC(tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream));
-    else TKC(tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream));
+    // SM footprint: the staged kernel runs one CTA per SM on min(SMs, tiles)
+    // SMs; the per-lane kernel is sized to the whole device
+    const int footprint = plan ? static_cast<int>(std::min<uint64_t>(
+                                     num_sms, (static_cast<uint64_t>(a.n) + plan->T - 1) / plan->T))
+                               : num_sms;
+    TKC(gated_coop_launch(device, num_sms, footprint, stream, [&] {
+        return plan ? tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream)
+                    : tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
+    }));
     if (e1) TKC(cudaEventRecord(e1, stream));
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
     TKC(cudaStreamSynchronize(stream));

@@ -477,6 +477,66 @@ class AnalysisPipeline:
         return out
 
 
+class BatchAnalyzer:
+    """End-to-end analysis of a batch of independent search spaces of any
+    shapes on one GPU (the C4 workload: many small landscapes back to back).
+    `workers` host threads each own a device handle (own CUDA stream) and pull
+    spaces from a shared queue -- upload, analyze_landscape, report read-back
+    -- so host-side launch and synchronisation latency of one space overlaps
+    the kernels of the others.  Results come back in input order.
+
+    items: sequence of (radix, fitness_ptr, ok_ptr) host buffers (ints, pinned
+    for asynchronous DMA); reports: None or per item a tuple of four pointers
+    (rank, fitness, ratio, pagerank) with room for n_minima entries."""
+
+    def __init__(self, device: int = 0, workers: int = 8, radix0=(2,)):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.workers = max(1, int(workers))
+        self.lands = [Landscape(list(radix0), device) for _ in range(self.workers)]
+        self.pool = ThreadPoolExecutor(self.workers)
+
+    def close(self):
+        self.pool.shutdown(wait=True)
+        for land in self.lands:
+            land.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def run(self, items, kind: int, reports=None, **analyze_kw):
+        import threading
+
+        out = [None] * len(items)
+        nxt = [0]
+        lock = threading.Lock()
+
+        def worker(w):
+            land = self.lands[w]
+            while True:
+                with lock:
+                    k = nxt[0]
+                    nxt[0] += 1
+                if k >= len(items):
+                    return
+                radix, fp, op = items[k]
+                if list(radix) != land.radix:
+                    land.reshape(radix)
+                land.load_dense_host_ptrs(fp, op)
+                s = land.analyze(kind, **analyze_kw)
+                if reports is not None and reports[k] is not None:
+                    land.report_copy_out_ptrs(s.f_opt, *reports[k])
+                out[k] = s
+
+        futs = [self.pool.submit(worker, w) for w in range(self.workers)]
+        for f in futs:
+            f.result()
+        return out
+
+
 # ------------------------------------------------- reference-shaped calls --
 
 def classify_points(cache: SearchSpaceCache, kind: int) -> PointCensus:

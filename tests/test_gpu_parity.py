@@ -349,3 +349,34 @@ def test_analysis_pipeline_matches_single_handle(tk):
         assert list(s.c_p[:16]) == w[3]
         for a, b in zip(bb, w[4]):
             assert np.array_equal(a[: w[2]], b)
+
+
+def test_batch_analyzer_concurrent_handles_match_sequential(tk):
+    """tk.BatchAnalyzer (several handles / streams in flight, cooperative
+    PageRank grids admitted concurrently by SM footprint) returns what one
+    handle analysing the spaces one after another returns."""
+    shapes = [[8, 6, 3, 3, 2], [12, 6, 8, 8, 2, 2], [4, 4, 3, 3, 3, 3, 4, 4, 2, 2],
+              [31, 11, 4, 2, 3], [6, 5, 4, 3, 2, 2, 2]]
+    tables = []
+    for k, radix in enumerate(shapes * 2):
+        fit, ok = O.gen_synthetic(radix, 0.1 * (k % 5), "rugged", k)
+        tables.append((radix, np.ascontiguousarray(fit, np.float64),
+                       np.ascontiguousarray(ok, np.uint8)))
+    want = []
+    for radix, fit, ok in tables:
+        with tk.Landscape(radix) as land:
+            land.load_dense(fit, ok)
+            s = land.analyze(tk.ADJACENT, node_limit=1 << 32)
+            want.append((s.iterations, s.n_edges, s.n_minima, list(s.c_p[:16]),
+                         land.report_rows(s.f_opt)))
+    bufs = [[np.empty(max(1, w[2]), dt) for dt in (np.uint64, np.float64, np.float64,
+                                                   np.float64)] for w in want]
+    items = [(radix, f.ctypes.data, o.ctypes.data) for radix, f, o in tables]
+    with tk.BatchAnalyzer(workers=4) as batch:
+        got = batch.run(items, tk.ADJACENT, [tuple(b.ctypes.data for b in bb) for bb in bufs],
+                        node_limit=1 << 32)
+    for s, w, bb in zip(got, want, bufs):
+        assert (s.iterations, s.n_edges, s.n_minima) == w[:3]
+        assert list(s.c_p[:16]) == w[3]
+        for a, b in zip(bb, w[4]):
+            assert np.array_equal(a[: w[2]], b)
