@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtk_landscape.so")
-SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_abi.cu"]
+SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_abi.cu"]
 HEADERS = ["tk_internal.cuh", "tk_kernels.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,6 +58,7 @@ VARIANTS = {
     "trace": ["-DTK_TRACE=1"],                        # per-tile timeline of block 0 (stderr)
     "p6": ["-DTK_PROD_WARPS=6"],
     "pw3": ["-DTK_PW_AHEAD=3"],
+    "hm1": ["-DTK_HAM_MINB=1"],
     "pw4": ["-DTK_PW_AHEAD=4"],
     # timing experiments (wrong results, fixed 29 iterations)
     "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],

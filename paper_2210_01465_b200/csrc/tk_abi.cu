@@ -447,9 +447,12 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
     const int footprint = plan ? static_cast<int>(std::min<uint64_t>(
                                      num_sms, (static_cast<uint64_t>(a.n) + plan->T - 1) / plan->T))
                                : num_sms;
-    TKC(gated_coop_launch(device, num_sms, footprint, stream, [&] {
-        return plan ? tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream)
-                    : tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
+    const bool ham_tiled = !plan && mode == tk::MODE_HAM && staged_enabled() &&
+                           tk::ham_tiled_supported(s);
+    TKC(gated_coop_launch(device, num_sms, ham_tiled ? num_sms : footprint, stream, [&] {
+        if (plan) return tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream);
+        if (ham_tiled) return tk::launch_pagerank_ham_tiled(s, wide, a, num_sms, &g, stream);
+        return tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
     }));
     if (e1) TKC(cudaEventRecord(e1, stream));
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));

@@ -130,6 +130,11 @@ constexpr int kPrThreads = 256;
 cudaError_t launch_pagerank(const DevShape& s, int mode, bool wide, const PrArgs& a,
                             int num_sms, int* grid_out, cudaStream_t stream);
 int pagerank_max_grid(int mode, bool wide, int num_sms);
+// Hamming: tiled contribution-only kernel (tk_hamming.cu) for shapes whose
+// digits align with 512-rank tiles; cudaErrorNotSupported otherwise
+bool ham_tiled_supported(const DevShape& s);
+cudaError_t launch_pagerank_ham_tiled(const DevShape& s, bool wide, const PrArgs& a, int num_sms,
+                                      int* grid_out, cudaStream_t stream);
 
 // ---- TMA-staged Adjacent kernels (tk_staged.cu) ------------------------------
 // A tile is T consecutive ranks [v0, v0+T).  The Adjacent neighbours of the tile
