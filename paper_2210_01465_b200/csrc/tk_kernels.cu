@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kBuildThreads) ffg_build_kernel(const DevShape
         const uint32_t u = tile * kBuildThreads + threadIdx.x;
         const bool valid = u < s.n;
         MW om = 0, im = 0;
-        bool tie = false;
+        bool notgt = false;  // some neighbour not strictly greater (== or NaN)
         uint8_t okv = 0;
         if (valid) {
             const double fu = a.fit[u];
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kBuildThreads) ffg_build_kernel(const DevShape
                           (static_cast<MW>(fh < fu) << (2 * i + 1));
                     im |= (static_cast<MW>(fl > fu) << i) |
                           (static_cast<MW>(fh > fu) << (d2 - i));
-                    tie |= (lo && fl == fu) || (hi && fh == fu);
+                    notgt |= (lo && !(fl > fu)) || (hi && !(fh > fu));
                 }
             } else {
                 for (int i = 0; i < s.dims; ++i) {
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kBuildThreads) ffg_build_kernel(const DevShape
                         const double f = a.fit[row + j * st];
                         om |= static_cast<MW>(f < fu) << b;
                         im |= static_cast<MW>(f > fu) << b;
-                        tie |= f == fu;
+                        notgt |= !(f > fu);
                         ++b;
                     }
                 }
@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(kBuildThreads) ffg_build_kernel(const DevShape
         const uint32_t deg = valid ? static_cast<uint32_t>(popc(om)) : 0u;
         const bool sink = valid && deg == 0;
         const bool fmin = sink && okv;
-        const bool strict = fmin && !tie;
+        // census minimum: ok and every neighbour strictly greater
+        const bool strict = fmin && !notgt;
         uint32_t etot = 0, mtot = 0;
         uint32_t epos = 0;
         if (EMIT) epos = block_exclusive_scan<kBuildThreads, uint32_t>(deg, etot, s_scan_e);

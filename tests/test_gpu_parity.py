@@ -141,6 +141,30 @@ def test_ffg_and_census_bit_exact(tk, radix, kind, gen):
     assert np.array_equal(cen.minima_ranks, rc["minima_ranks"])
 
 
+@pytest.mark.parametrize("path", ["staged", "v1"])
+def test_ffg_with_nan_fitness_bit_exact(tk, monkeypatch, path):
+    """NaN fitness values (all fp64 comparisons with them are false): the FFG
+    edges (f(v) < f(u)), sinks and minima stay bit-exact, and the strict census
+    keeps its definition -- every neighbour strictly greater -- so a NaN node or
+    a NaN neighbour is never a census minimum."""
+    if path == "v1":
+        monkeypatch.setenv("TK_KERNELS", "v1")
+    radix = [8, 6, 6, 4, 4]
+    fit, ok = O.gen_iid(O.space_size(radix), 0.2, 7)
+    fit = fit.copy()
+    fit[[5, 777, 2048]] = np.nan
+    ref = O.build_ffg(radix, fit, ok, O.ADJACENT, node_limit=1 << 32, nthreads=8)
+    off, tg, sk, mn = gpu_ffg(tk, radix, fit, ok, O.ADJACENT)
+    assert np.array_equal(off, ref["offsets"]) and np.array_equal(tg, ref["targets"])
+    assert np.array_equal(sk, ref["is_sink"]) and np.array_equal(mn, ref["minima"])
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(O.ADJACENT, node_limit=1 << 32, emit_csr=False)
+        cen = land.census()
+    rc = O.census(radix, fit, ok, O.ADJACENT)
+    assert np.array_equal(cen.minima_ranks, rc["minima_ranks"])
+
+
 def test_census_with_ties(tk):
     # SPEC.md:387 constant space: no strict minima, every ok node an FFG minimum
     radix = [4, 3, 5]
