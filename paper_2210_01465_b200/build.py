@@ -59,6 +59,7 @@ VARIANTS = {
     "p6": ["-DTK_PROD_WARPS=6"],
     "pw3": ["-DTK_PW_AHEAD=3"],
     "hm1": ["-DTK_HAM_MINB=1"],
+    "hu4": ["-DTK_HAM_UNROLL=4"],
     "pw4": ["-DTK_PW_AHEAD=4"],
     # timing experiments (wrong results, fixed 29 iterations)
     "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],

@@ -5,13 +5,13 @@
 // sum(m_i - 1) = 50 per node on C5.  Staging them is out of reach (the far
 // lines of one 512-rank tile are ~36 ranges, ~150 KB), so this kernel gathers
 // with coalesced loads -- consecutive lanes hold consecutive ranks, so every
-// line load of a warp is one 256-byte run.  Measured on C5 (B200): ~14.7 ms
-// per iteration, the same as the per-lane kernel (tk_kernels.cu MODE_HAM) it
-// replaces; both are bound by gather latency and by L2 misses on the lines of
-// the two slowest dimensions (DRAM ~190 B per rank and iteration), which no
-// tile order avoids -- every order leaves the slowest digit's lines spanning
-// most of the space.  What this kernel adds is the contribution-only
-// iteration (no per-iteration r' traffic) and no per-rank digit decode.
+// line load of a warp is one 256-byte run.  Measured on C5 (B200): ~11.7 ms
+// per iteration against 14.7 for the per-lane kernel (tk_kernels.cu MODE_HAM)
+// it replaces; both are bound by gather latency (DRAM at ~20 % of peak even
+// though the lines of the slowest dimensions miss L2, ~190 B per rank and
+// iteration).  Unrolling the per-value loops by two beats one, four and
+// eight (445 / 570 / 544 / 854 ms on C5); re-ordering the tile sweep did not
+// help (profiles/r01_ab_log.md).
 //
 // Tiles are 512 consecutive ranks aligned to 512.  For the shapes this kernel
 // takes (StagePlan-style digit classes, see tk_kernels.cuh) each digit is
@@ -41,6 +41,10 @@ namespace tk {
 namespace {
 
 constexpr int kHT = 512;  // ranks per tile = threads per CTA
+#ifndef TK_HAM_UNROLL
+#define TK_HAM_UNROLL 2
+#endif
+constexpr int kHamUnroll = TK_HAM_UNROLL;  // values per dimension whose loads issue together
 #ifndef TK_HAM_MINB
 #define TK_HAM_MINB 2
 #endif
@@ -92,7 +96,7 @@ __device__ __forceinline__ double ham_in_sum(const DevShape& s, const double* c,
         const uint32_t st = s.stride[i], xi = x[i];
         const double* row = c + (v - xi * st);
         const unsigned long long mi = mask >> s.base[i];
-#pragma unroll 4
+#pragma unroll kHamUnroll
         for (uint32_t j = 0; j < xi; ++j)
             if ((mi >> j) & 1ull) acc = __dadd_rn(acc, __ldca(row + j * st));
     }
@@ -102,7 +106,7 @@ __device__ __forceinline__ double ham_in_sum(const DevShape& s, const double* c,
         const uint32_t st = s.stride[i], xi = x[i], m = s.radix[i];
         const double* row = c + (v - xi * st);
         const unsigned long long mi = mask >> (s.base[i] + xi);  // value j at bit j - xi - 1
-#pragma unroll 4
+#pragma unroll kHamUnroll
         for (uint32_t j = xi + 1; j < m; ++j)
             if ((mi >> (j - xi - 1)) & 1ull) acc = __dadd_rn(acc, __ldca(row + j * st));
     }
