@@ -432,3 +432,33 @@ def test_batch_analyzer_concurrent_handles_match_sequential(tk):
         assert list(s.c_p[:16]) == w[3]
         for a, b in zip(bb, w[4]):
             assert np.array_equal(a[: w[2]], b)
+
+
+@pytest.mark.slow
+def test_c5_full_size_parity(tk):
+    """BASELINE C5 at its full size (113,246,208 configurations, 1.02e9 edges):
+    the device-generated table, the FFG CSR and minima bit-exact against the
+    oracle, PageRank with the same iteration count and within 1e-12 relative
+    L1, and the C_p curve within 1e-9 -- the bench workload itself."""
+    import os
+
+    radix = [8, 8, 8, 6, 6, 6, 4, 4, 4, 4, 2, 2]
+    threads = os.cpu_count() or 8
+    with tk.Landscape(radix) as land:
+        land.generate(0, 0.10, 5)
+        s = land.analyze(tk.ADJACENT, node_limit=1 << 32, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+        r = land.pagerank_vector()
+        fit, ok = land.fitness()
+    assert (s.n_edges, s.n_minima, s.iterations) == (1023020492, 5917841, 29)
+    rf, ro = O.gen_iid(O.space_size(radix), 0.10, 5, nthreads=threads)
+    assert np.array_equal(fit.view(np.uint64), rf.view(np.uint64)) and np.array_equal(ok, ro)
+    del rf, ro
+    ref = O.analyze(radix, fit, ok, O.ADJACENT, nthreads=threads, node_limit=1 << 32)
+    g = ref["ffg"]
+    assert np.array_equal(off, g["offsets"]) and np.array_equal(tg, g["targets"])
+    assert np.array_equal(sk, g["is_sink"]) and np.array_equal(mn, g["minima"])
+    assert s.iterations == ref["iterations"]
+    assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
+    for k, c in ref["c_p_curve"]:
+        assert abs(s.c_p[k] - c) <= CP_ATOL
