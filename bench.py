@@ -508,9 +508,14 @@ def run_sharded(args, wl, kind):
     S.connect_peers_ipc(shard, allgather)
     stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device("cuda", local))
 
+    # NCCL: partials all-reduced in device memory, one host sync per iteration;
+    # gloo stages CUDA tensors through the host, so there the host loop is faster
+    loop = (S.device_pagerank_loop(shard, f"cuda:{local}")
+            if backend == "nccl" and not os.environ.get("TK_HOST_LOOP") else None)
+
     def step():
         return S.analyze_sharded([shard], allreduce, allgather, kind, DAMPING, TOL, MAX_ITER,
-                                 P_MAX)
+                                 P_MAX, pagerank_loop=loop)
 
     for _ in range(max(3, args.warmup)):
         res = step()

@@ -175,6 +175,14 @@ int tk_shard_pagerank_init(tk_land* land, double damping, double* dangling);
 int tk_shard_pagerank_step(tk_land* land, double dangling_total, double damping,
                            double* residual, double* dangling, double* sum);
 /* nums[n_p] and den: the shard's C_p numerators / denominator */
+/* Device-side iteration control: the same init / step, asynchronous on the
+ * handle's stream (tk_land_stream).  d_partials (device, 3 doubles) receives
+ * this shard's (L1 change, dangling mass, sum of r'); the step reads the
+ * all-reduced totals of the previous step from d_totals (device) -- the caller
+ * all-reduces d_partials in place on that stream (NCCL) between calls. */
+int tk_shard_pagerank_init_dev(tk_land* land, double damping, double* d_partials);
+int tk_shard_pagerank_step_dev(tk_land* land, const double* d_totals, double damping,
+                               double* d_partials);
 int tk_shard_centrality(tk_land* land, double f_opt, const double* p, int n_p, double* nums,
                         double* den);
 /* the shard's slice [lo, hi) of the current rank vector */

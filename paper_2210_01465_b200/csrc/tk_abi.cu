@@ -1168,6 +1168,49 @@ int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, do
     return TK_OK;
 }
 
+// Device-side iteration control: the same init / step as
+// above, enqueued on the handle's stream without any host synchronisation.
+// Partials land in caller device memory (three doubles), so a collective can
+// all-reduce them in place on that stream and the next step reads the reduced
+// dangling mass from there; the host reads back only what its stop test needs.
+int tk_shard_pagerank_init_dev(tk_land* l, double damping, double* d_partials) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    if (int st = check_pr_args(damping, 1.0, 1)) return st;
+    if (!d_partials) return fail(TK_EINVAL, "shard init: null partials buffer");
+    TKC(set_dev(l));
+    TKC(ensure(l->r0, (l->n + kPad) * 8));
+    TKC(ensure(l->r1, (l->n + kPad) * 8));
+    TKC(ensure(l->part, static_cast<size_t>(l->num_sms) * 4 * 3 * 8));
+    TKC(cudaMemsetAsync(l->part.p, 0, static_cast<size_t>(l->num_sms) * 4 * 3 * 8, l->stream));
+    tk::PrArgs a = shard_pr_args(l, damping);
+    TKC(tk::launch_pagerank_shard_init(l->shape, shard_info(l), a, l->om.as<uint32_t>(),
+                                       l->part.as<double>(), d_partials, l->num_sms, l->stream));
+    l->shard_cur = 0;
+    l->shard_pr = true;
+    l->iterations = 0;
+    return TK_OK;
+}
+
+int tk_shard_pagerank_step_dev(tk_land* l, const double* d_totals, double damping,
+                               double* d_partials) {
+    if (int st = check_land(l)) return st;
+    if (int st = shard_ready(l)) return st;
+    if (!l->shard_pr) return fail(TK_ESTATE, "shard step before tk_shard_pagerank_init");
+    if (!d_totals || !d_partials) return fail(TK_EINVAL, "shard step: null device buffer");
+    TKC(set_dev(l));
+    tk::StagePlan plan{};
+    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan))
+        return fail(TK_EINVAL, "shard step: no staging plan for this shape");
+    tk::PrArgs a = shard_pr_args(l, damping);
+    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a, l->om.as<uint32_t>(),
+                                       l->shard_cur, 0.0, l->part.as<double>(), d_partials,
+                                       l->num_sms, l->stream, d_totals));
+    l->shard_cur ^= 1;
+    ++l->iterations;
+    return TK_OK;
+}
+
 int tk_shard_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* nums,
                         double* den) {
     if (int st = check_land(l)) return st;

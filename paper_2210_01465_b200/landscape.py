@@ -378,6 +378,16 @@ class Landscape:
                                              C.byref(s)))
         return r.value, d.value, s.value
 
+    def shard_pagerank_init_dev(self, damping, partials_ptr: int):
+        """Asynchronous on this handle's stream; partials to device memory."""
+        _check(self.L.tk_shard_pagerank_init_dev(self.h, damping, C.c_void_p(partials_ptr)))
+
+    def shard_pagerank_step_dev(self, totals_ptr: int, damping, partials_ptr: int):
+        """Asynchronous on this handle's stream: reads the previous step's
+        all-reduced totals from device memory, writes this shard's partials."""
+        _check(self.L.tk_shard_pagerank_step_dev(self.h, C.c_void_p(totals_ptr), damping,
+                                                 C.c_void_p(partials_ptr)))
+
     def shard_centrality(self, f_opt, ps):
         p = np.ascontiguousarray(ps, np.float64)
         nums = np.zeros(p.shape[0], np.float64)

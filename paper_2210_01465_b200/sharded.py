@@ -47,7 +47,7 @@ class NonConvergenceError(RuntimeError):
 
 
 def analyze_sharded(shards, allreduce_sum, allgather, kind, damping=0.85, tol=1e-10,
-                    max_iter=100000, p_max_percent=15):
+                    max_iter=100000, p_max_percent=15, pagerank_loop=None):
     """Drive `shards` (the shards of this process) through one sharded
     analyze_landscape.
 
@@ -56,6 +56,9 @@ def analyze_sharded(shards, allreduce_sum, allgather, kind, damping=0.85, tol=1e
                    -> (res, dang, sum), centrality(f_opt, ps) -> (nums, den)
     allreduce_sum  f(np.ndarray) -> elementwise sum over all processes
     allgather      f(list) -> concatenation of every process's list
+    pagerank_loop  optional f(damping, tol, max_iter) -> (iterations, residual,
+                   sum, converged) replacing the host-driven iteration below
+                   (device_pagerank_loop: partials all-reduced in device memory)
     """
     edges = minima = 0
     for s in shards:
@@ -70,18 +73,21 @@ def analyze_sharded(shards, allreduce_sum, allgather, kind, damping=0.85, tol=1e
         raise RuntimeError("NoFeasiblePoint: search space has no ok entry")
     f_opt, opt_rank = min(feas)  # lexicographic: lowest rank among equal fitness
 
-    dang = allreduce_sum(np.array([sum(s.pagerank_init(damping) for s in shards)]))[0]
-    it, res, total = 0, 0.0, 0.0
-    converged = False
-    while it < max_iter:
-        part = np.zeros(3)
-        for s in shards:
-            part += np.asarray(s.pagerank_step(dang, damping), np.float64)
-        res, dang, total = allreduce_sum(part)
-        it += 1
-        if res < tol:
-            converged = True
-            break
+    if pagerank_loop is not None:
+        it, res, total, converged = pagerank_loop(damping, tol, max_iter)
+    else:
+        dang = allreduce_sum(np.array([sum(s.pagerank_init(damping) for s in shards)]))[0]
+        it, res, total = 0, 0.0, 0.0
+        converged = False
+        while it < max_iter:
+            part = np.zeros(3)
+            for s in shards:
+                part += np.asarray(s.pagerank_step(dang, damping), np.float64)
+            res, dang, total = allreduce_sum(part)
+            it += 1
+            if res < tol:
+                converged = True
+                break
     if not converged:
         raise NonConvergenceError(it, res)
 
@@ -138,6 +144,40 @@ def connect_peers_ipc(shard, allgather):
     """One shard per process: exchange CUDA IPC handles of the replicas."""
     handles = allgather([shard.land.ipc_handles()])
     shard.land.open_peers(handles)
+
+
+def device_pagerank_loop(shard, device):
+    """PageRank iteration control with the partial sums kept in device memory
+    (one shard per process, torch.distributed initialised).  Per iteration:
+    the step kernel and its partial reduction are enqueued on the shard's
+    stream, the three partials are all-reduced in place on that stream (NCCL
+    under torchrun), and the host reads back only the reduced totals for its
+    stop test -- one synchronisation per iteration instead of three host
+    round trips.  The next step reads the reduced dangling mass from device
+    memory.  Returns the pagerank_loop callable for analyze_sharded."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device(device))
+    bufs = [torch.zeros(3, dtype=torch.float64, device=device) for _ in range(2)]
+
+    def loop(damping, tol, max_iter):
+        it, res, total, k = 0, 0.0, 0.0, 0
+        with torch.cuda.stream(stream):
+            shard.land.shard_pagerank_init_dev(damping, bufs[0].data_ptr())
+            dist.all_reduce(bufs[0])
+            while it < max_iter:
+                shard.land.shard_pagerank_step_dev(bufs[k].data_ptr(), damping,
+                                                   bufs[k ^ 1].data_ptr())
+                dist.all_reduce(bufs[k ^ 1])
+                res, _, total = (float(x) for x in bufs[k ^ 1].cpu())
+                k ^= 1
+                it += 1
+                if res < tol:
+                    return it, res, total, True
+        return it, res, total, False
+
+    return loop
 
 
 def torch_collectives(device=None):

@@ -251,7 +251,7 @@ def test_virtual_gpu_shards_match_oracle(radix, nshards):
         s.land.close()
 
 
-def _gpu_ipc_worker(rank, world, port, out):
+def _gpu_ipc_worker(rank, world, port, out, dev_loop=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -264,7 +264,8 @@ def _gpu_ipc_worker(rank, world, port, out):
         shard.land.load_dense(fit, ok)
         allreduce, allgather = S.torch_collectives()
         S.connect_peers_ipc(shard, allgather)
-        res = S.analyze_sharded([shard], allreduce, allgather, O.ADJACENT)
+        loop = S.device_pagerank_loop(shard, "cuda:0") if dev_loop else None
+        res = S.analyze_sharded([shard], allreduce, allgather, O.ADJACENT, pagerank_loop=loop)
         r = shard.land.shard_pagerank_vector(shard.lo, shard.hi)
         out.put((rank, res, shard.lo, r))
         dist.barrier()  # peers stay mapped until everyone is done
@@ -274,9 +275,12 @@ def _gpu_ipc_worker(rank, world, port, out):
 
 
 @pytest.mark.gpu
-def test_two_processes_one_gpu_cuda_ipc():
+@pytest.mark.parametrize("dev_loop", [False, True])
+def test_two_processes_one_gpu_cuda_ipc(dev_loop):
     """The multi-process path end to end on one device: two ranks, replicas
-    mapped with CUDA IPC, remote pushes through the mapped pointers."""
+    mapped with CUDA IPC, remote pushes through the mapped pointers; with the
+    host-driven iteration and with device-side iteration control (partials
+    all-reduced in device memory)."""
     import torch
 
     if not torch.cuda.is_available():
@@ -286,7 +290,7 @@ def test_two_processes_one_gpu_cuda_ipc():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_ipc_worker, args=(r, 2, port, q, dev_loop)) for r in range(2)]
     for p in procs:
         p.start()
     got = {}
