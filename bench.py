@@ -598,6 +598,8 @@ def run_sharded(args, wl, kind):
             "gpu_launches": args.steps * (4 + 2 * (it + 1) + 2),
             "clocks": clk,
         }))
+    if loop is not None:
+        loop.close()
     shard.land.close()
     dist.barrier()
     dist.destroy_process_group()

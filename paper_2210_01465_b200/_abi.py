@@ -30,7 +30,7 @@ EXPORTS = [
     "tk_pagerank_csr", "tk_proportion_of_centrality",
     "tk_land_set_shard", "tk_land_replica_ptrs", "tk_land_set_peer_ptrs", "tk_land_ipc_handles",
     "tk_land_open_peers", "tk_shard_optimum", "tk_shard_pagerank_init", "tk_shard_pagerank_step",
-    "tk_shard_pagerank_init_dev", "tk_shard_pagerank_step_dev",
+    "tk_shard_pagerank_init_dev", "tk_shard_pagerank_step_dev", "tk_shard_pagerank_rewind",
     "tk_shard_centrality", "tk_shard_pagerank_copy_out",
 ]
 
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
         "tk_shard_pagerank_step": (I, [P, D, D, PD, PD, PD]),
         "tk_shard_pagerank_init_dev": (I, [P, D, P]),
         "tk_shard_pagerank_step_dev": (I, [P, P, D, P]),
+        "tk_shard_pagerank_rewind": (I, [P]),
         "tk_shard_centrality": (I, [P, D, P, I, P, PD]),
         "tk_shard_pagerank_copy_out": (I, [P, P]),
     }

@@ -1211,6 +1211,17 @@ int tk_shard_pagerank_step_dev(tk_land* l, const double* d_totals, double dampin
     return TK_OK;
 }
 
+// Drop the last tk_shard_pagerank_step_dev (a speculative step issued before
+// the previous step's stop test was read): its r' went to the other parity
+// buffer, so the previous iterate is intact; only the bookkeeping rewinds.
+int tk_shard_pagerank_rewind(tk_land* l) {
+    if (int st = check_land(l)) return st;
+    if (!l->shard_pr || l->iterations < 1) return fail(TK_ESTATE, "shard rewind: no step to drop");
+    l->shard_cur ^= 1;
+    --l->iterations;
+    return TK_OK;
+}
+
 int tk_shard_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* nums,
                         double* den) {
     if (int st = check_land(l)) return st;

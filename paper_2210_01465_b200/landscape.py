@@ -388,6 +388,9 @@ class Landscape:
         _check(self.L.tk_shard_pagerank_step_dev(self.h, C.c_void_p(totals_ptr), damping,
                                                  C.c_void_p(partials_ptr)))
 
+    def shard_pagerank_rewind(self):
+        _check(self.L.tk_shard_pagerank_rewind(self.h))
+
     def shard_centrality(self, f_opt, ps):
         p = np.ascontiguousarray(ps, np.float64)
         nums = np.zeros(p.shape[0], np.float64)

@@ -146,38 +146,72 @@ def connect_peers_ipc(shard, allgather):
     shard.land.open_peers(handles)
 
 
-def device_pagerank_loop(shard, device):
+class DevicePagerankLoop:
     """PageRank iteration control with the partial sums kept in device memory
-    (one shard per process, torch.distributed initialised).  Per iteration:
-    the step kernel and its partial reduction are enqueued on the shard's
-    stream, the three partials are all-reduced in place on that stream (NCCL
-    under torchrun), and the host reads back only the reduced totals for its
-    stop test -- one synchronisation per iteration instead of three host
-    round trips.  The next step reads the reduced dangling mass from device
-    memory.  Returns the pagerank_loop callable for analyze_sharded."""
-    import torch
-    import torch.distributed as dist
+    (one shard per process, torch.distributed initialised).  Step i's kernel
+    and partial reduction are enqueued on the shard's stream and its three
+    partials all-reduced in place on that stream (NCCL under torchrun); the
+    reduced totals are copied to pinned host memory behind an event, and step
+    i+1 -- which reads the reduced dangling mass from device memory -- is
+    enqueued before the host waits for that event.  So the stop test of step
+    i overlaps step i+1.  When step i converges, step i+1 was speculative: it
+    wrote r' into the other parity buffer, and tk_shard_pagerank_rewind drops
+    it (every rank speculates identically, so the collectives stay matched).
+    An instance is the pagerank_loop callable of analyze_sharded; close() it
+    before the process group and the CUDA context go away."""
 
-    stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device(device))
-    bufs = [torch.zeros(3, dtype=torch.float64, device=device) for _ in range(2)]
+    def __init__(self, shard, device):
+        import torch
 
-    def loop(damping, tol, max_iter):
-        it, res, total, k = 0, 0.0, 0.0, 0
-        with torch.cuda.stream(stream):
-            shard.land.shard_pagerank_init_dev(damping, bufs[0].data_ptr())
-            dist.all_reduce(bufs[0])
-            while it < max_iter:
-                shard.land.shard_pagerank_step_dev(bufs[k].data_ptr(), damping,
-                                                   bufs[k ^ 1].data_ptr())
-                dist.all_reduce(bufs[k ^ 1])
-                res, _, total = (float(x) for x in bufs[k ^ 1].cpu())
-                k ^= 1
-                it += 1
-                if res < tol:
-                    return it, res, total, True
-        return it, res, total, False
+        self.shard = shard
+        self.stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device(device))
+        self.bufs = [torch.zeros(3, dtype=torch.float64, device=device) for _ in range(3)]
+        self.host = [torch.zeros(3, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        self.evs = [torch.cuda.Event() for _ in range(2)]
 
-    return loop
+    def _launch(self, i, damping):
+        """step i: totals in bufs[i % 3] -> partials in bufs[(i + 1) % 3]"""
+        import torch.distributed as dist
+
+        dst = self.bufs[(i + 1) % 3]
+        self.shard.land.shard_pagerank_step_dev(self.bufs[i % 3].data_ptr(), damping,
+                                                dst.data_ptr())
+        dist.all_reduce(dst)
+        self.host[i % 2].copy_(dst, non_blocking=True)
+        self.evs[i % 2].record(self.stream)
+
+    def __call__(self, damping, tol, max_iter):
+        import torch
+        import torch.distributed as dist
+
+        with torch.cuda.stream(self.stream):
+            self.shard.land.shard_pagerank_init_dev(damping, self.bufs[0].data_ptr())
+            dist.all_reduce(self.bufs[0])
+            self._launch(0, damping)
+            i = 0
+            while True:
+                if i + 1 < max_iter:
+                    self._launch(i + 1, damping)  # speculative until step i's test is read
+                self.evs[i % 2].synchronize()
+                res, _, total = (float(x) for x in self.host[i % 2])
+                if res < tol or i + 1 >= max_iter:
+                    if i + 1 < max_iter:
+                        self.stream.synchronize()
+                        self.shard.land.shard_pagerank_rewind()
+                    return i + 1, res, total, res < tol
+                i += 1
+
+    def close(self):
+        import torch
+
+        self.stream.synchronize()
+        self.bufs = self.host = self.evs = None
+        torch.cuda.synchronize()
+
+
+def device_pagerank_loop(shard, device):
+    """DevicePagerankLoop(shard, device) -- see there."""
+    return DevicePagerankLoop(shard, device)
 
 
 def torch_collectives(device=None):

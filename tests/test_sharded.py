@@ -267,6 +267,8 @@ def _gpu_ipc_worker(rank, world, port, out, dev_loop=False):
         loop = S.device_pagerank_loop(shard, "cuda:0") if dev_loop else None
         res = S.analyze_sharded([shard], allreduce, allgather, O.ADJACENT, pagerank_loop=loop)
         r = shard.land.shard_pagerank_vector(shard.lo, shard.hi)
+        if loop is not None:
+            loop.close()
         out.put((rank, res, shard.lo, r))
         dist.barrier()  # peers stay mapped until everyone is done
         shard.land.close()
