@@ -277,13 +277,15 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
             emit = 0;
         }
         TKC(ensure(l->om, (n + kPad) * 4));
-        TKC(ensure(l->tile_cnt, static_cast<size_t>(nt) * 8 + 16));
-        TKC(ensure(l->tile_base, (static_cast<size_t>(nt) + 1) * 16));
+        // per-warp-slot (32 ranks) counts and their exclusive scans
+        const size_t ns = static_cast<size_t>(nt) * (plan.T / 32);
+        TKC(ensure(l->tile_cnt, ns * 8 + 16));
+        TKC(ensure(l->tile_base, (ns + 1) * 16));
         a.om = l->om.as<uint32_t>();
         a.tile_e = l->tile_cnt.as<uint32_t>();
-        a.tile_m = a.tile_e + nt;
+        a.tile_m = a.tile_e + ns;
         a.ebase = l->tile_base.as<unsigned long long>();
-        a.mbase = a.ebase + (nt + 1);
+        a.mbase = a.ebase + (ns + 1);
         TKC(ensure(l->opt_part, static_cast<size_t>(l->num_sms) * 4 * 16));
         a.opt_part_f = l->opt_part.as<double>();
         a.opt_part_r = reinterpret_cast<unsigned long long*>(a.opt_part_f + l->num_sms * 4);
@@ -292,8 +294,8 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
         a.opt_has = &ds->has;
         l->opt_ready = true;
         TKC(tk::launch_ffg_build_staged(s, plan, emit != 0, a, l->num_sms, l->stream));
-        TKC(cudaMemcpyAsync(ds->totals + 0, a.ebase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
-        TKC(cudaMemcpyAsync(ds->totals + 1, a.mbase + nt, 8, cudaMemcpyDeviceToDevice, l->stream));
+        TKC(cudaMemcpyAsync(ds->totals + 0, a.ebase + ns, 8, cudaMemcpyDeviceToDevice, l->stream));
+        TKC(cudaMemcpyAsync(ds->totals + 1, a.mbase + ns, 8, cudaMemcpyDeviceToDevice, l->stream));
         l->staged = true;
     } else {
         if (l->sharded)
