@@ -874,9 +874,54 @@ cudaError_t launch_csr_prepare(uint32_t n, const unsigned long long* offsets,
     return cudaGetLastError();
 }
 
+// Wide variant for long inputs (the N/32 warp-slot counts of the FFG build):
+// 4096 elements per look-back tile (16 per thread), so the serial look-back
+// chain is 16x shorter than with one element per thread.
+constexpr int kScanItems = 16;
+__global__ void __launch_bounds__(256) scan_u32_wide_kernel(
+    const uint32_t* __restrict__ in, uint32_t n, unsigned long long* __restrict__ out,
+    unsigned long long* status, unsigned int* tile_counter, uint32_t ntiles) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_base;
+    __shared__ unsigned long long s_scan[8];
+    constexpr uint32_t kSpan = 256 * kScanItems;
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= ntiles) return;
+        const uint32_t u0 = tile * kSpan + threadIdx.x * kScanItems;
+        uint32_t v[kScanItems];
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            v[k] = u0 + k < n ? __ldg(in + u0 + k) : 0u;
+            sum += v[k];
+        }
+        unsigned long long tot;
+        const unsigned long long pos = block_exclusive_scan<256, unsigned long long>(sum, tot, s_scan);
+        if (threadIdx.x == 0) s_base = lookback(status, tile, tot);
+        __syncthreads();
+        unsigned long long run = s_base + pos;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (u0 + k < n) out[u0 + k] = run;
+            if (u0 + k == n - 1) out[n] = run + v[k];
+            run += v[k];
+        }
+        __syncthreads();
+    }
+}
+
 cudaError_t launch_exclusive_scan_u32(const uint32_t* in, uint32_t n, unsigned long long* out,
                                       unsigned long long* status, unsigned int* tile_counter,
                                       uint32_t ntiles, int num_sms, cudaStream_t stream) {
+    if (n > 65536) {  // `ntiles` (and the status array) were sized for 256-element tiles
+        const uint32_t wt = (n + 256 * kScanItems - 1) / (256 * kScanItems);
+        scan_u32_wide_kernel<<<grid_for(wt, 1, num_sms * 8), 256, 0, stream>>>(
+            in, n, out, status, tile_counter, wt);
+        return cudaGetLastError();
+    }
     scan_u32_kernel<<<grid_for(ntiles, 1, num_sms * 8), 256, 0, stream>>>(in, n, out, status,
                                                                           tile_counter, ntiles);
     return cudaGetLastError();
