@@ -182,7 +182,7 @@ def run_batch(args, wl, kind):
         dist.barrier()
         dist.destroy_process_group()
     return 0
-KERNELS_PER_STEP = 6  # ffg_build, optimum x2, pagerank, cp_partial, cp_final
+KERNELS_PER_STEP = 8  # ffg_count, optimum_final, 2 slot scans, ffg_fill, pagerank, cp_partial, cp_final
 DAMPING, TOL, MAX_ITER, P_MAX = 0.85, 1e-10, 100000, 15
 
 
