@@ -47,7 +47,11 @@ constexpr unsigned long long kEmpty = ~0ull;
 
 // Locality-preserving open-addressing slot: 32 consecutive keys share one
 // hashed 32-slot run, so a warp probing consecutive ranks reads one
-// contiguous 256 B segment of keys; runs are scattered by mix64.
+// contiguous 256 B segment of keys; runs are scattered by mix64.  A key whose
+// slot is taken probes the same position of the next runs (stride 32), so a
+// group displaced by another group moves to the next run together instead of
+// walking slot by slot through the occupied run (C5 valid set, unordered
+// keys: 17 -> ~2 atomic probes per key).
 __device__ __forceinline__ unsigned long long hslot(unsigned long long key,
                                                    unsigned long long mask) {
     return ((mix64(key >> 5) << 5) | (key & 31ull)) & mask;
@@ -127,7 +131,7 @@ __global__ void hash_build_kernel(const unsigned long long* __restrict__ keys,
                 atomicExch(err, 2);
                 break;
             }
-            s = (s + 1) & mask;
+            s = (s + 32) & mask;  // next run, same lane position
         }
     }
 }
@@ -149,7 +153,7 @@ __global__ void hash_densify_kernel(const unsigned long long* __restrict__ hkeys
                 break;
             }
             if (k == kEmpty) break;
-            s = (s + 1) & mask;
+            s = (s + 32) & mask;  // next run, same lane position
         }
         fit[u] = f;
         ok[u] = good;
@@ -175,7 +179,7 @@ __global__ void hash_lookup_kernel(const unsigned long long* __restrict__ hkeys,
                     break;
                 }
                 if (k == kEmpty) break;
-                s = (s + 1) & mask;
+                s = (s + 32) & mask;  // next run, same lane position
             }
         }
         out[i] = f;
