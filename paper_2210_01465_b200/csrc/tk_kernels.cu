@@ -717,21 +717,28 @@ __global__ void __launch_bounds__(256) cp_partial_kernel(
 
 // raw = 1 writes the sums (n_p numerators, then the denominator) instead of
 // the ratios: a shard's partials for the cross-GPU sum.
-__global__ void cp_final_kernel(const double* __restrict__ part, int n_p, int nblocks,
-                                double* __restrict__ c_p, int* degenerate, int raw) {
-    __shared__ double s_den;
-    if (threadIdx.x == 0) {
-        double den = 0.0;
-        for (int b = 0; b < nblocks; ++b) den = __dadd_rn(den, part[static_cast<size_t>(n_p) * nblocks + b]);
-        s_den = den;
-        *degenerate = !(den > 0.0);
-        if (raw) c_p[n_p] = den;
+// One block per p (block n_p: the denominator only): each block sums the
+// partial row of its p and the denominator row with a fixed thread-strided
+// assignment and a fixed tree, so the result is deterministic run to run.
+__global__ void __launch_bounds__(256) cp_final_kernel(const double* __restrict__ part, int n_p,
+                                                       int nblocks, double* __restrict__ c_p,
+                                                       int* degenerate, int raw) {
+    __shared__ double s_red[8];
+    const int p = blockIdx.x;
+    double num = 0.0, den = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 256) {
+        den = __dadd_rn(den, part[static_cast<size_t>(n_p) * nblocks + b]);
+        if (p < n_p) num = __dadd_rn(num, part[static_cast<size_t>(p) * nblocks + b]);
     }
-    __syncthreads();
-    for (int p = threadIdx.x; p < n_p; p += blockDim.x) {
-        double num = 0.0;
-        for (int b = 0; b < nblocks; ++b) num = __dadd_rn(num, part[static_cast<size_t>(p) * nblocks + b]);
-        c_p[p] = raw ? num : __ddiv_rn(num, s_den);
+    den = block_sum<256>(den, s_red);
+    num = block_sum<256>(num, s_red);
+    if (threadIdx.x == 0) {
+        if (p == n_p) {
+            *degenerate = !(den > 0.0);
+            if (raw) c_p[n_p] = den;
+        } else {
+            c_p[p] = raw ? num : __ddiv_rn(num, den);
+        }
     }
 }
 
@@ -999,7 +1006,8 @@ cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* 
     }
     dim3 grid(kCpBlocks, (n_p + kCpPerRow - 1) / kCpPerRow);
     cp_partial_kernel<<<grid, 256, 0, stream>>>(minima, m, fit, r, P, part);
-    cp_final_kernel<<<1, 128, 0, stream>>>(part, n_p, kCpBlocks, c_p_out, degenerate, raw ? 1 : 0);
+    cp_final_kernel<<<n_p + 1, 256, 0, stream>>>(part, n_p, kCpBlocks, c_p_out, degenerate,
+                                                 raw ? 1 : 0);
     return cudaGetLastError();
 }
 

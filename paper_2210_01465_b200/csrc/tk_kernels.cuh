@@ -197,7 +197,7 @@ cudaError_t launch_pagerank_shard_step(const DevShape& s, const StagePlan& p, co
                                        cudaStream_t stream, const double* dtot = nullptr);
 
 // ---- C_p and report -------------------------------------------------------
-constexpr int kCpBlocks = 148;
+constexpr int kCpBlocks = 148 * 8;  // enough warps to hide the dependent minima -> (f, r) gathers
 // minima == nullptr: fit/r are already per-minimum arrays of length m.
 // raw: c_p_out receives n_p numerators then the denominator (n_p + 1 values).
 cudaError_t launch_centrality(const uint32_t* minima, uint64_t m, const double* fit,
