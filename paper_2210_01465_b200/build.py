@@ -79,13 +79,17 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     deps.append(os.path.join(ROOT, "include", "tk_landscape.h"))
     if not force and not _stale(out, deps):
         return out
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
+    objs, cmds = [], []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", f"{'_' + variant if variant else ''}.o"))
-        cmd = [nvcc(), *flags((["-Xptxas", "-v"] if verbose else []) + VARIANTS[variant]), "-c",
-               os.path.join(CSRC, src), "-o", obj]
-        subprocess.run(cmd, check=True)
+        cmds.append([nvcc(), *flags((["-Xptxas", "-v"] if verbose else []) + VARIANTS[variant]),
+                     "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
+    with ThreadPoolExecutor(len(cmds)) as ex:  # translation units compile independently
+        for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            f.result()
     cmd = [nvcc(), *ARCH, "-ccbin", host_cxx(), "-shared", "-o", out, *objs]
     subprocess.run(cmd, check=True)
     return out
