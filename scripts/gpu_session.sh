@@ -15,6 +15,11 @@ if [[ $WHAT == all || $WHAT == tests || $WHAT == quick ]]; then
   timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 \
       python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/sanitizer_smoke.log" 2>&1
   echo "exit=$?" >> "$OUT/sanitizer_smoke.log"
+  for tool in racecheck synccheck initcheck; do
+    timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 \
+        python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/sanitizer_$tool.log" 2>&1
+    echo "exit=$?" >> "$OUT/sanitizer_$tool.log"
+  done
   timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > "$OUT/pytest_gpu.log" 2>&1
   echo "exit=$?" >> "$OUT/pytest_gpu.log"
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
