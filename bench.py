@@ -572,7 +572,10 @@ def run_sharded(args, wl, kind):
     n = shard.land.n
     it = runs[-1]["iterations"]
     peaks, peak_src = measured_peaks()
-    per_gpu_bytes = (20 * n + 36 * n * it) / world  # PageRank algorithmic bytes per GPU
+    # PageRank algorithmic bytes per GPU: init 12 B/rank, per step 20 B/rank
+    # (packed word 4, each c read once 8, c' written 8; contribution-only),
+    # r rebuilt once at the end 20 B/rank
+    per_gpu_bytes = (32 * n + 20 * n * it) / world
     ms_step = t_ms / args.steps
     if rank == 0:
         print(json.dumps({

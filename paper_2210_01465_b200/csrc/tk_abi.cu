@@ -140,6 +140,7 @@ struct tk_land {
     std::vector<void*> ipc_opened;
     int shard_cur = 0;          // parity holding the current iterate
     bool shard_pr = false;      // tk_shard_pagerank_init done
+    bool shard_r_fresh = false; // r0 holds the rank vector of the current iterate
 };
 
 namespace {
@@ -502,8 +503,21 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     return TK_OK;
 }
 
+// Sharded PageRank stores contributions only; the shard's rank vector is
+// rebuilt into r0 (shard_materialize_kernel) the first time a reader needs it
+// after a step.  Enqueued on the handle's stream ahead of the reader.
+cudaError_t shard_refresh_r(tk_land* l) {
+    if (!l->sharded || !l->shard_pr || l->shard_r_fresh) return cudaSuccess;
+    const double* c = l->shard_cur ? l->c1.as<double>() : l->c0.as<double>();
+    cudaError_t e = tk::launch_shard_materialize(l->shard_lo, l->shard_hi, l->pw.as<uint32_t>(), c,
+                                                 l->r0.as<double>(), l->num_sms, l->stream);
+    if (e == cudaSuccess) l->shard_r_fresh = true;
+    return e;
+}
+
+// (sharded handles: call shard_refresh_r first)
 const double* pr_result(const tk_land* l) {
-    if (l->sharded && l->shard_pr) return l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
+    if (l->sharded && l->shard_pr) return l->r0.as<double>();
     return l->pr_parity ? l->r1.as<double>() : l->r0.as<double>();
 }
 
@@ -515,6 +529,7 @@ int do_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* c_
     TKC(ensure(l->cp_part, static_cast<size_t>(TK_MAX_CP + 1) * tk::kCpBlocks * 8));
     TKC(ensure(l->cp_out, TK_MAX_CP * 8));
     Small* ds = l->small.as<Small>();
+    TKC(shard_refresh_r(l));
     TKC(tk::launch_centrality(l->minima.as<uint32_t>(), l->n_minima, l->fit.as<double>(),
                               pr_result(l), p, n_p, f_opt, l->cp_part.as<double>(),
                               l->cp_out.as<double>(), &ds->degenerate, l->stream));
@@ -916,6 +931,7 @@ int tk_pagerank_copy_out(tk_land* l, double* r) {
     if (int st = check_land(l)) return st;
     if (!l->pr_done) return fail(TK_ESTATE, "pagerank_copy_out: no converged PageRank");
     TKC(set_dev(l));
+    TKC(shard_refresh_r(l));
     TKC(cudaMemcpyAsync(r, pr_result(l), l->n * 8, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
     return TK_OK;
@@ -940,6 +956,7 @@ int tk_report_copy_out(tk_land* l, double f_opt, uint64_t* ranks, double* fitnes
     double* df = reinterpret_cast<double*>(dr + m);
     double* dfr = df + m;
     double* dp = dfr + m;
+    TKC(shard_refresh_r(l));
     TKC(tk::launch_report(l->minima.as<uint32_t>(), m, l->fit.as<double>(), pr_result(l), f_opt,
                           dr, df, dfr, dp, l->stream));
     if (ranks) TKC(cudaMemcpyAsync(ranks, dr, m * 8, cudaMemcpyDeviceToHost, l->stream));
@@ -1130,7 +1147,6 @@ int tk_shard_pagerank_init(tk_land* l, double damping, double* dangling) {
     if (int st = check_pr_args(damping, 1.0, 1)) return st;
     TKC(set_dev(l));
     TKC(ensure(l->r0, (l->n + kPad) * 8));
-    TKC(ensure(l->r1, (l->n + kPad) * 8));
     TKC(ensure(l->part, static_cast<size_t>(l->num_sms) * 4 * 3 * 8));
     Small* ds = l->small.as<Small>();
     tk::PrArgs a = shard_pr_args(l, damping);
@@ -1141,6 +1157,7 @@ int tk_shard_pagerank_init(tk_land* l, double damping, double* dangling) {
     if (dangling) *dangling = l->hsmall->totals_f[1];
     l->shard_cur = 0;
     l->shard_pr = true;
+    l->shard_r_fresh = false;
     l->iterations = 0;
     return TK_OK;
 }
@@ -1152,7 +1169,7 @@ int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, do
     if (!l->shard_pr) return fail(TK_ESTATE, "shard step before tk_shard_pagerank_init");
     TKC(set_dev(l));
     tk::StagePlan plan{};
-    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan))
+    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false))
         return fail(TK_EINVAL, "shard step: no staging plan for this shape");
     Small* ds = l->small.as<Small>();
     tk::PrArgs a = shard_pr_args(l, damping);
@@ -1163,6 +1180,7 @@ int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, do
     TKC(cudaMemcpyAsync(l->hsmall->totals_f, ds->totals_f, 24, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
     l->shard_cur ^= 1;
+    l->shard_r_fresh = false;
     ++l->iterations;
     if (residual) *residual = l->hsmall->totals_f[0];
     if (dangling) *dangling = l->hsmall->totals_f[1];
@@ -1182,7 +1200,6 @@ int tk_shard_pagerank_init_dev(tk_land* l, double damping, double* d_partials) {
     if (!d_partials) return fail(TK_EINVAL, "shard init: null partials buffer");
     TKC(set_dev(l));
     TKC(ensure(l->r0, (l->n + kPad) * 8));
-    TKC(ensure(l->r1, (l->n + kPad) * 8));
     TKC(ensure(l->part, static_cast<size_t>(l->num_sms) * 4 * 3 * 8));
     TKC(cudaMemsetAsync(l->part.p, 0, static_cast<size_t>(l->num_sms) * 4 * 3 * 8, l->stream));
     tk::PrArgs a = shard_pr_args(l, damping);
@@ -1190,6 +1207,7 @@ int tk_shard_pagerank_init_dev(tk_land* l, double damping, double* d_partials) {
                                        l->part.as<double>(), d_partials, l->num_sms, l->stream));
     l->shard_cur = 0;
     l->shard_pr = true;
+    l->shard_r_fresh = false;
     l->iterations = 0;
     return TK_OK;
 }
@@ -1202,13 +1220,14 @@ int tk_shard_pagerank_step_dev(tk_land* l, const double* d_totals, double dampin
     if (!d_totals || !d_partials) return fail(TK_EINVAL, "shard step: null device buffer");
     TKC(set_dev(l));
     tk::StagePlan plan{};
-    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan))
+    if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false))
         return fail(TK_EINVAL, "shard step: no staging plan for this shape");
     tk::PrArgs a = shard_pr_args(l, damping);
     TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a, l->om.as<uint32_t>(),
                                        l->shard_cur, 0.0, l->part.as<double>(), d_partials,
                                        l->num_sms, l->stream, d_totals));
     l->shard_cur ^= 1;
+    l->shard_r_fresh = false;
     ++l->iterations;
     return TK_OK;
 }
@@ -1220,6 +1239,7 @@ int tk_shard_pagerank_rewind(tk_land* l) {
     if (int st = check_land(l)) return st;
     if (!l->shard_pr || l->iterations < 1) return fail(TK_ESTATE, "shard rewind: no step to drop");
     l->shard_cur ^= 1;
+    l->shard_r_fresh = false;
     --l->iterations;
     return TK_OK;
 }
@@ -1239,7 +1259,8 @@ int tk_shard_centrality(tk_land* l, double f_opt, const double* p, int n_p, doub
     TKC(ensure(l->cp_part, static_cast<size_t>(TK_MAX_CP + 1) * tk::kCpBlocks * 8));
     TKC(ensure(l->cp_out, (TK_MAX_CP + 1) * 8));
     Small* ds = l->small.as<Small>();
-    const double* r = l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
+    TKC(shard_refresh_r(l));
+    const double* r = pr_result(l);
     TKC(tk::launch_centrality(l->minima.as<uint32_t>(), l->n_minima, l->fit.as<double>(), r, p, n_p,
                               f_opt, l->cp_part.as<double>(), l->cp_out.as<double>(),
                               &ds->degenerate, l->stream, true));
@@ -1254,7 +1275,8 @@ int tk_shard_pagerank_copy_out(tk_land* l, double* r_slice) {
     if (int st = check_land(l)) return st;
     if (!l->sharded || !l->shard_pr) return fail(TK_ESTATE, "no sharded PageRank state");
     TKC(set_dev(l));
-    const double* r = l->shard_cur ? l->r1.as<double>() : l->r0.as<double>();
+    TKC(shard_refresh_r(l));
+    const double* r = pr_result(l);
     TKC(cudaMemcpyAsync(r_slice, r + l->shard_lo, (l->shard_hi - l->shard_lo) * 8,
                         cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));

@@ -184,7 +184,8 @@ cudaError_t launch_pagerank_staged(const DevShape& s, const StagePlan& p, const 
 // Shard steps (one launch per PageRank iteration, no grid barrier): ranks
 // [sh.lo, sh.hi); c' is stored into the local replica and, for ranks with an
 // out-neighbour owned by another shard, into that shard's replica.
-// init: r0, c0 (parity 0) + dangling partial;  step: reads parity `cur`,
+// Contribution-only: no rank vector is stored per step (c = r / outdeg, r for
+// a sink).  init: c0 (parity 0) + dangling partial;  step: reads parity `cur`,
 // writes parity cur^1.  Partials land in out3[0..2] (res, dangling, sum).
 cudaError_t launch_pagerank_shard_init(const DevShape& s, const ShardInfo& sh, const PrArgs& a,
                                        const uint32_t* om, double* part, double* out3,
@@ -195,6 +196,9 @@ cudaError_t launch_pagerank_shard_step(const DevShape& s, const StagePlan& p, co
                                        const PrArgs& a, const uint32_t* om, int cur, double dn,
                                        double* part, double* out3, int num_sms,
                                        cudaStream_t stream, const double* dtot = nullptr);
+// r[v] over the shard's ranks [lo, hi) from its contributions c (shard_materialize_kernel)
+cudaError_t launch_shard_materialize(uint64_t lo, uint64_t hi, const uint32_t* pw, const double* c,
+                                    double* r, int num_sms, cudaStream_t stream);
 
 // ---- C_p and report -------------------------------------------------------
 constexpr int kCpBlocks = 148 * 8;  // enough warps to hide the dependent minima -> (f, r) gathers
