@@ -184,8 +184,10 @@ int tk_shard_pagerank_init_dev(tk_land* land, double damping, double* d_partials
 int tk_shard_pagerank_step_dev(tk_land* land, const double* d_totals, double damping,
                                double* d_partials);
 /* Undo the bookkeeping of the last step (after a speculative step past the
- * stop: that step wrote r' to the other parity buffer, the previous iterate
- * stays where it was). */
+ * stop: that step wrote its contributions to the other parity buffer, the
+ * previous iterate stays where it was).  The shard steps store contributions
+ * only; readers of the rank vector (copy_out, centrality, report) rebuild it
+ * from the current iterate's contributions on first use. */
 int tk_shard_pagerank_rewind(tk_land* land);
 int tk_shard_centrality(tk_land* land, double f_opt, const double* p, int n_p, double* nums,
                         double* den);

@@ -155,7 +155,7 @@ class DevicePagerankLoop:
     i+1 -- which reads the reduced dangling mass from device memory -- is
     enqueued before the host waits for that event.  So the stop test of step
     i overlaps step i+1.  When step i converges, step i+1 was speculative: it
-    wrote r' into the other parity buffer, and tk_shard_pagerank_rewind drops
+    wrote its contributions into the other parity buffer, and tk_shard_pagerank_rewind drops
     it (every rank speculates identically, so the collectives stay matched).
     An instance is the pagerank_loop callable of analyze_sharded; close() it
     before the process group and the CUDA context go away."""
