@@ -1174,7 +1174,7 @@ int tk_shard_pagerank_step(tk_land* l, double dangling_total, double damping, do
     Small* ds = l->small.as<Small>();
     tk::PrArgs a = shard_pr_args(l, damping);
     const double dn = dangling_total / static_cast<double>(l->n);
-    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a, l->om.as<uint32_t>(),
+    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a,
                                        l->shard_cur, dn, l->part.as<double>(), ds->totals_f,
                                        l->num_sms, l->stream));
     TKC(cudaMemcpyAsync(l->hsmall->totals_f, ds->totals_f, 24, cudaMemcpyDeviceToHost, l->stream));
@@ -1223,7 +1223,7 @@ int tk_shard_pagerank_step_dev(tk_land* l, const double* d_totals, double dampin
     if (!tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false))
         return fail(TK_EINVAL, "shard step: no staging plan for this shape");
     tk::PrArgs a = shard_pr_args(l, damping);
-    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a, l->om.as<uint32_t>(),
+    TKC(tk::launch_pagerank_shard_step(l->shape, plan, shard_info(l), a,
                                        l->shard_cur, 0.0, l->part.as<double>(), d_partials,
                                        l->num_sms, l->stream, d_totals));
     l->shard_cur ^= 1;

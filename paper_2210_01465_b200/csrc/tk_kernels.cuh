@@ -193,7 +193,7 @@ cudaError_t launch_pagerank_shard_init(const DevShape& s, const ShardInfo& sh, c
 // dtot (optional, device): previous step's all-reduced totals; D/N is formed
 // on the device from dtot[1] instead of taking dn
 cudaError_t launch_pagerank_shard_step(const DevShape& s, const StagePlan& p, const ShardInfo& sh,
-                                       const PrArgs& a, const uint32_t* om, int cur, double dn,
+                                       const PrArgs& a, int cur, double dn,
                                        double* part, double* out3, int num_sms,
                                        cudaStream_t stream, const double* dtot = nullptr);
 // r[v] over the shard's ranks [lo, hi) from its contributions c (shard_materialize_kernel)
