@@ -586,6 +586,7 @@ def run_sharded(args, wl, kind):
             "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"],
                        "nodes": n, "edges": e, "minima": runs[-1]["n_minima"],
                        "pagerank_iterations": it, "parallelism": f"keyrange{world}",
+                       "shard_push": os.environ.get("TK_SHARD_PUSH", "crossing"),
                        "l2": "inputs larger than L2"},
             "s_per_space": round(ms_step / 1e3, 5),
             "roofline": {"bound": "hbm", "achieved": round(per_gpu_bytes / (ms_step / 1e3) / 1e9, 1),

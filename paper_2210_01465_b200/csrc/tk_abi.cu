@@ -1108,6 +1108,11 @@ tk::ShardInfo shard_info(const tk_land* l) {
         sh.peer_c[0][g] = static_cast<double*>(l->peer_c0[g]);
         sh.peer_c[1][g] = static_cast<double*>(l->peer_c1[g]);
     }
+    // TK_SHARD_PUSH=edges: push c' only along out-edges (half the NVLink
+    // volume, out-mask load + partial-sector stores); default: along every
+    // crossing direction (Exchange volume)
+    const char* e = std::getenv("TK_SHARD_PUSH");
+    sh.edges_om = (e && std::strcmp(e, "edges") == 0) ? l->om.as<uint32_t>() : nullptr;
     return sh;
 }
 

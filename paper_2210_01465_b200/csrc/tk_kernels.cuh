@@ -72,6 +72,7 @@ struct ShardInfo {
     uint32_t lo, hi;
     unsigned long long chunk_magic;  // fdiv magic of the chunk length
     double* peer_c[2][kMaxShards];   // [parity][rank] replica base pointers
+    const uint32_t* edges_om;        // non-null: push along out-edges only (out-masks)
 };
 constexpr int kBuildThreads = 256;
 cudaError_t launch_ffg_build(const DevShape& s, int mode, bool wide, bool emit,

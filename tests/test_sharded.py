@@ -228,10 +228,13 @@ class LocalGroup:
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("push", ["crossing", "edges"])  # TK_SHARD_PUSH
 @pytest.mark.parametrize("nshards", [1, 2, 3, 8])
 @pytest.mark.parametrize("radix", [[8, 8, 6, 6, 4, 4, 2], [6, 5, 4, 4, 3], [2, 9, 7, 5, 3]])
-def test_virtual_gpu_shards_match_oracle(radix, nshards):
+def test_virtual_gpu_shards_match_oracle(radix, nshards, push, monkeypatch):
     import torch
+
+    monkeypatch.setenv("TK_SHARD_PUSH", push)
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
