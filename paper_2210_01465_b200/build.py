@@ -61,6 +61,7 @@ VARIANTS = {
     "hm1": ["-DTK_HAM_MINB=1"],
     "hu4": ["-DTK_HAM_UNROLL=4"],
     "pw4": ["-DTK_PW_AHEAD=4"],
+    "s3": ["-DTK_MAX_STAGES=3"],  # at most 3 pipeline stages (more L1 left)
     # timing experiments (wrong results, fixed 29 iterations)
     "xnodim0": ["-DTK_X_ITERS=29", "-DTK_X_NODIM0=1"],
     "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
