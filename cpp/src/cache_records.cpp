@@ -3,7 +3,8 @@
 // Record semantics follow cache_io.cpp (/root/reference/proj/src/cache_io.cpp:
 // 33-75): a record is ok iff it has a numeric "times" array or a numeric
 // "time"; everything else, and every configuration without a record, is a
-// failed node (kFailFitness).
+// failed node (kFailFitness).  Absent configurations are how constraints
+// appear in a cache, so a partial cache is the normal input here.
 #include <fstream>
 #include <memory>
 #include <vector>
@@ -102,9 +103,11 @@ CentralityReport analyze_cache_file(const std::string& path, NeighbourhoodKind k
         configs.insert(configs.end(), x.begin(), x.end());
         fitness.push_back(mean);
     }
-    if (records != space.size())
-        throw Error("landscape analysis needs a complete cache (" + std::to_string(records) + " of " +
-                    std::to_string(space.size()) + " configurations present)");
+    // A configuration without a record is infeasible: Kernel Tuner never writes
+    // the configurations its restrictions exclude, and the reference models
+    // constraints as fail fitness (cache.cpp:9-16 leaves an absent
+    // rank at kFailFitness, not ok).  The valid set is exactly the ok records.
+    (void)records;
     if (space_out) *space_out = space;
     std::vector<std::uint32_t> radix(dims);
     for (std::size_t i = 0; i < dims; ++i) radix[i] = static_cast<std::uint32_t>(space.list_size(i));

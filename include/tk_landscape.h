@@ -93,13 +93,16 @@ void* tk_land_stream(tk_land* land);
 int tk_land_kernel_info(const tk_land* land, int* staged_build, int* staged_pagerank,
                         int* pagerank_grid, float* ms_build, float* ms_pagerank);
 
-/* SearchSpaceCache::mean/ok (cache.hpp:42-48): rank-indexed fitness (failed
- * entries carry kFailFitness = 1e10, cache.hpp:15) and ok flags.  The cache
- * must be complete. */
+/* SearchSpaceCache::mean/ok (cache.hpp:42-48): rank-indexed fitness and ok
+ * flags.  The cache must be complete.  Failed entries are forced
+ * to kFailFitness = 1e10 (cache.hpp:15, cache.cpp:49-53); an ok mean >= 1e10
+ * -> TK_EINVAL. */
 int tk_land_load_dense(tk_land* land, const double* fitness, const uint8_t* ok, int mem);
-/* Valid set as (key = rank, fitness) pairs: an open-addressing hash table is
- * built on the device and every absent key becomes a failed node (1e10).
- * Duplicate keys or keys >= N -> TK_EINVAL. */
+/* Valid set as (key = rank, fitness) pairs (cache_io.cpp:79-112: constrained
+ * configurations are absent or failed entries).  Keys are ranks < N,
+ * so the valid set is scattered straight into the rank-indexed table; every
+ * absent key becomes a failed node (1e10).  Duplicate keys, keys >= N, or an
+ * ok mean >= 1e10 (cache.hpp:15) -> TK_EINVAL. */
 int tk_land_load_sparse(tk_land* land, const uint64_t* keys, const double* fitness,
                         uint64_t n_valid, int mem);
 /* Same, with configurations as index vectors (row-major int32[n_valid][dims]),
@@ -108,7 +111,9 @@ int tk_land_load_configs(tk_land* land, const int32_t* configs, const double* fi
                          uint64_t n_valid, int mem);
 int tk_land_generate(tk_land* land, int gen, double fail_fraction, uint64_t seed);
 int tk_land_copy_fitness(tk_land* land, double* fitness, uint8_t* ok);
-/* Hash lookup of arbitrary keys in the last sparse table: fitness or 1e10. */
+/* Lookup of arbitrary keys in the valid set of the loaded table through a GPU
+ * open-addressing hash table (built on the first lookup after a load):
+ * fitness and found = 1 for an ok rank, 1e10 and found = 0 otherwise. */
 int tk_land_lookup(tk_land* land, const uint64_t* keys, uint64_t n, double* fitness,
                    uint8_t* found);
 

@@ -87,6 +87,79 @@ static int check_space(uint32_t dims, const uint32_t* radix, int kind) {
  * ranks carry 1e10).  A2: u->v iff v in N(u) and f(v) < f(u), strict.
  * A3: row order is neighbour_ranks order.  A4: minima = ok && outdeg == 0,
  * ascending.  A9: N > node_limit -> InvalidArgument (OR_ELIMIT). */
+/* Per-thread static chunk [lo, hi) of the node range. */
+static void chunk_of(uint64_t n, int nt, int t, uint64_t* lo, uint64_t* hi) {
+    const uint64_t q = n / (uint64_t)nt, r = n % (uint64_t)nt;
+    *lo = (uint64_t)t * q + ((uint64_t)t < r ? (uint64_t)t : r);
+    *hi = *lo + q + ((uint64_t)t < r ? 1 : 0);
+}
+
+/* nbr_ranks with the digits of `rank` already known (an odometer walks them
+ * through a chunk, so the per-node div/mod of src/space.cpp:171-173 happens
+ * once per chunk); same order as nbr_ranks. */
+static uint32_t nbr_ranks_digits(uint32_t dims, const uint32_t* radix, const uint64_t* strides,
+                                 uint64_t rank, const uint32_t* x, int kind, uint64_t* out) {
+    uint32_t k = 0;
+    for (uint32_t i = 0; i < dims; ++i) {
+        const uint64_t s = strides[i];
+        const uint32_t xi = x[i], m = radix[i];
+        const uint64_t base = rank - (uint64_t)xi * s;
+        if (kind == OR_HAMMING) {
+            for (uint32_t j = 0; j < m; ++j)
+                if (j != xi) out[k++] = base + (uint64_t)j * s;
+        } else {
+            if (xi > 0) out[k++] = rank - s;
+            if (xi + 1 < m) out[k++] = rank + s;
+        }
+    }
+    return k;
+}
+
+static void digits_of(uint32_t dims, const uint64_t* strides, const uint32_t* radix,
+                      uint64_t rank, uint32_t* x) {
+    for (uint32_t i = 0; i < dims; ++i) x[i] = (uint32_t)((rank / strides[i]) % radix[i]);
+}
+
+static void odometer_next(uint32_t dims, const uint32_t* radix, uint32_t* x) {
+    for (uint32_t i = dims; i-- > 0;) {
+        if (++x[i] < radix[i]) return;
+        x[i] = 0;
+    }
+}
+
+/* Out-degree of every node into deg[u] (deg may alias offsets + 1). */
+static void ffg_degrees(uint32_t dims, const uint32_t* radix, const uint64_t* strides, uint64_t n,
+                        const double* fit, int kind, uint32_t maxnb, uint64_t* deg, int nt) {
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nt)
+#endif
+    {
+        int t = 0, T = 1;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+        T = omp_get_num_threads();
+#endif
+        uint64_t lo, hi;
+        chunk_of(n, T, t, &lo, &hi);
+        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
+        uint32_t x[OR_MAX_DIMS];
+        if (lo < hi) digits_of(dims, strides, radix, lo, x);
+        for (uint64_t u = lo; u < hi; ++u) {
+            const uint32_t k = nbr_ranks_digits(dims, radix, strides, u, x, kind, nb);
+            uint64_t d = 0;
+            const double fu = fit[u];
+            for (uint32_t j = 0; j < k; ++j) d += fit[nb[j]] < fu;
+            deg[u] = d;
+            odometer_next(dims, radix, x);
+        }
+        free(nb);
+    }
+}
+
+/* landscape.hpp:26-45.  A1: nodes are all N ranks (failed
+ * ranks carry 1e10).  A2: u->v iff v in N(u) and f(v) < f(u), strict.
+ * A3: row order is neighbour_ranks order.  A4: minima = ok && outdeg == 0,
+ * ascending.  A9: N > node_limit -> InvalidArgument (OR_ELIMIT). */
 int or_ffg_count(uint32_t dims, const uint32_t* radix, const double* fit,
                  const uint8_t* ok, int kind, uint64_t node_limit,
                  uint64_t* n_edges, uint64_t* n_minima, int nthreads) {
@@ -95,22 +168,30 @@ int or_ffg_count(uint32_t dims, const uint32_t* radix, const double* fit,
     const uint64_t n = or_space_strides(dims, radix, strides);
     if (n > node_limit || n > 0xffffffffull) return OR_ELIMIT;
     const uint32_t maxnb = or_max_neighbours(dims, radix, kind);
+    const int nt = nthreads > 0 ? nthreads : 1;
     uint64_t edges = 0, minima = 0;
 #ifdef _OPENMP
-#pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1) reduction(+ : edges, minima)
+#pragma omp parallel num_threads(nt) reduction(+ : edges, minima)
 #endif
     {
-        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
+        int t = 0, T = 1;
 #ifdef _OPENMP
-#pragma omp for schedule(static)
+        t = omp_get_thread_num();
+        T = omp_get_num_threads();
 #endif
-        for (int64_t ui = 0; ui < (int64_t)n; ++ui) {
-            const uint64_t u = (uint64_t)ui;
-            const uint32_t k = nbr_ranks(dims, radix, strides, u, kind, nb);
+        uint64_t lo, hi;
+        chunk_of(n, T, t, &lo, &hi);
+        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
+        uint32_t x[OR_MAX_DIMS];
+        if (lo < hi) digits_of(dims, strides, radix, lo, x);
+        for (uint64_t u = lo; u < hi; ++u) {
+            const uint32_t k = nbr_ranks_digits(dims, radix, strides, u, x, kind, nb);
             uint64_t deg = 0;
-            for (uint32_t j = 0; j < k; ++j) deg += fit[nb[j]] < fit[u];
+            const double fu = fit[u];
+            for (uint32_t j = 0; j < k; ++j) deg += fit[nb[j]] < fu;
             edges += deg;
             minima += (deg == 0 && ok[u]);
+            odometer_next(dims, radix, x);
         }
         free(nb);
     }
@@ -127,49 +208,67 @@ int or_ffg_fill(uint32_t dims, const uint32_t* radix, const double* fit,
     const uint64_t n = or_space_strides(dims, radix, strides);
     const uint32_t maxnb = or_max_neighbours(dims, radix, kind);
     const int nt = nthreads > 0 ? nthreads : 1;
-    (void)nt;
     /* pass 1: out-degrees into offsets[u+1] */
     offsets[0] = 0;
+    ffg_degrees(dims, radix, strides, n, fit, kind, maxnb, offsets + 1, nt);
+    /* exclusive scan -> CSR offsets; minima compaction in ascending rank
+     * (two-level: per-chunk totals, then each chunk rescans from its base) */
+    uint64_t part_e[257], part_m[257];
+    const int T = nt < 256 ? nt : 256;
 #ifdef _OPENMP
-#pragma omp parallel num_threads(nt)
+#pragma omp parallel for num_threads(T) schedule(static, 1)
 #endif
-    {
-        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
-#ifdef _OPENMP
-#pragma omp for schedule(static)
-#endif
-        for (int64_t ui = 0; ui < (int64_t)n; ++ui) {
-            const uint64_t u = (uint64_t)ui;
-            const uint32_t k = nbr_ranks(dims, radix, strides, u, kind, nb);
-            uint64_t deg = 0;
-            for (uint32_t j = 0; j < k; ++j) deg += fit[nb[j]] < fit[u];
-            offsets[u + 1] = deg;
+    for (int t = 0; t < T; ++t) {
+        uint64_t lo, hi, e = 0, m = 0;
+        chunk_of(n, T, t, &lo, &hi);
+        for (uint64_t u = lo; u < hi; ++u) {
+            e += offsets[u + 1];
+            m += offsets[u + 1] == 0 && ok[u];
         }
-        free(nb);
+        part_e[t + 1] = e;
+        part_m[t + 1] = m;
     }
-    /* exclusive scan -> CSR offsets; minima compaction in ascending rank */
-    uint64_t m = 0;
-    for (uint64_t u = 0; u < n; ++u) {
-        const uint64_t deg = offsets[u + 1];
-        offsets[u + 1] = offsets[u] + deg;
-        is_sink[u] = deg == 0;
-        if (deg == 0 && ok[u]) minima[m++] = (uint32_t)u;
+    part_e[0] = part_m[0] = 0;
+    for (int t = 0; t < T; ++t) {
+        part_e[t + 1] += part_e[t];
+        part_m[t + 1] += part_m[t];
+    }
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+#endif
+    for (int t = 0; t < T; ++t) {
+        uint64_t lo, hi, e = part_e[t], m = part_m[t];
+        chunk_of(n, T, t, &lo, &hi);
+        for (uint64_t u = lo; u < hi; ++u) {
+            const uint64_t deg = offsets[u + 1];
+            offsets[u + 1] = e + deg;
+            e += deg;
+            is_sink[u] = deg == 0;
+            if (deg == 0 && ok[u]) minima[m++] = (uint32_t)u;
+        }
     }
     /* pass 2: targets in neighbour_ranks order */
 #ifdef _OPENMP
 #pragma omp parallel num_threads(nt)
 #endif
     {
-        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
+        int t = 0, Tn = 1;
 #ifdef _OPENMP
-#pragma omp for schedule(static)
+        t = omp_get_thread_num();
+        Tn = omp_get_num_threads();
 #endif
-        for (int64_t ui = 0; ui < (int64_t)n; ++ui) {
-            const uint64_t u = (uint64_t)ui;
-            const uint32_t k = nbr_ranks(dims, radix, strides, u, kind, nb);
+        uint64_t lo, hi;
+        chunk_of(n, Tn, t, &lo, &hi);
+        uint64_t* nb = (uint64_t*)malloc(sizeof(uint64_t) * (maxnb + 1));
+        uint32_t x[OR_MAX_DIMS];
+        if (lo < hi) digits_of(dims, strides, radix, lo, x);
+        for (uint64_t u = lo; u < hi; ++u) {
+            const uint32_t k = nbr_ranks_digits(dims, radix, strides, u, x, kind, nb);
             uint64_t o = offsets[u];
+            const double fu = fit[u];
             for (uint32_t j = 0; j < k; ++j)
-                if (fit[nb[j]] < fit[u]) targets[o++] = (uint32_t)nb[j];
+                if (fit[nb[j]] < fu) targets[o++] = (uint32_t)nb[j];
+            odometer_next(dims, radix, x);
         }
         free(nb);
     }
@@ -195,7 +294,6 @@ int or_pagerank(uint64_t n, const uint64_t* offsets, const uint32_t* targets,
     if (!(damping >= 0.0 && damping <= 1.0) || !(tol > 0.0) || max_iter < 1)
         return OR_EINVAL;
     const int nt = nthreads > 0 ? nthreads : 1;
-    (void)nt;
     const uint64_t e = offsets[n];
     /* stable transpose: in-CSR with sources ascending inside each row */
     uint64_t* in_off = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
@@ -208,13 +306,67 @@ int or_pagerank(uint64_t n, const uint64_t* offsets, const uint32_t* targets,
         free(in_off); free(src); free(c); free(r); free(rn); free(cursor);
         return OR_EINVAL;
     }
-    for (uint64_t i = 0; i < e; ++i) in_off[targets[i] + 1]++;
-    for (uint64_t v = 0; v < n; ++v) in_off[v + 1] += in_off[v];
-    memcpy(cursor, in_off, sizeof(uint64_t) * n);
-    for (uint64_t u = 0; u < n; ++u)
-        for (uint64_t i = offsets[u]; i < offsets[u + 1]; ++i)
-            src[cursor[targets[i]]++] = (uint32_t)u;
+    /* parallel stable transpose: count in-degrees (atomic), scan, scatter
+     * with an atomic cursor per row, then sort each (short) row so the
+     * sources come out ascending -- the result equals the serial transpose */
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t i = 0; i < (int64_t)e; ++i)
+        __atomic_fetch_add(&in_off[targets[i] + 1], 1, __ATOMIC_RELAXED);
+    {
+        uint64_t part[257];
+        const int T = nt < 256 ? nt : 256;
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+#endif
+        for (int t = 0; t < T; ++t) {
+            uint64_t lo, hi, acc = 0;
+            chunk_of(n, T, t, &lo, &hi);
+            for (uint64_t v = lo; v < hi; ++v) acc += in_off[v + 1];
+            part[t + 1] = acc;
+        }
+        part[0] = 0;
+        for (int t = 0; t < T; ++t) part[t + 1] += part[t];
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+#endif
+        for (int t = 0; t < T; ++t) {
+            uint64_t lo, hi, acc = part[t];
+            chunk_of(n, T, t, &lo, &hi);
+            for (uint64_t v = lo; v < hi; ++v) {
+                acc += in_off[v + 1];
+                in_off[v + 1] = acc;
+            }
+        }
+    }
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t vi = 0; vi < (int64_t)n; ++vi) cursor[vi] = in_off[vi];
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t ui = 0; ui < (int64_t)n; ++ui)
+        for (uint64_t i = offsets[ui]; i < offsets[ui + 1]; ++i)
+            src[__atomic_fetch_add(&cursor[targets[i]], 1, __ATOMIC_RELAXED)] = (uint32_t)ui;
     free(cursor);
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nt) schedule(static)
+#endif
+    for (int64_t vi = 0; vi < (int64_t)n; ++vi) {
+        uint32_t* row = src + in_off[vi];
+        const uint64_t len = in_off[vi + 1] - in_off[vi];
+        for (uint64_t a = 1; a < len; ++a) {
+            const uint32_t key = row[a];
+            uint64_t b = a;
+            while (b > 0 && row[b - 1] > key) {
+                row[b] = row[b - 1];
+                --b;
+            }
+            row[b] = key;
+        }
+    }
 
     const double nd = (double)n;
     const double teleport = (1.0 - damping) / nd;

@@ -105,8 +105,8 @@ struct tk_land {
 
     DevBuf fit, ok;
     bool loaded = false;
-    DevBuf hkeys, hvals, staging_keys, staging_vals, staging_cfg;
-    uint64_t hcap = 0;
+    DevBuf hkeys, hvals, staging_keys, staging_vals, staging_cfg, claimed;
+    uint64_t hcap = 0;  // 0 = no valid-set hash table for the loaded table yet
 
     bool built = false, emitted = false;
     int kind = TK_ADJACENT, mode = 0;
@@ -547,36 +547,58 @@ cudaMemcpyKind h2x(int mem) {
     return mem == TK_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
 }
 
+// Valid (key, fitness) pairs -> the dense rank-indexed table (perfect hash:
+// keys are ranks < N).  Absent keys are failed points (SPEC.md:82,
+// cache_io.cpp:79-112).
 int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const double* dvals,
                         uint64_t nv) {
+    TKC(ensure(l->fit, (l->n + kPad) * 8));
+    TKC(ensure(l->ok, l->n + kPad));
+    TKC(ensure(l->claimed, ((l->n + 31) / 32) * 4));
+    l->hcap = 0;
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
+    TKC(tk::launch_load_valid(dkeys, dvals, nv, static_cast<uint32_t>(l->n), l->fit.as<double>(),
+                              l->ok.as<uint8_t>(), l->claimed.as<unsigned int>(), &ds->err,
+                              l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    l->built = l->pr_done = false;
+    l->loaded = false;
+    l->opt_ready = false;
+    const int err = l->hsmall->err;
+    if (err & 1) return fail(TK_EINVAL, "load: configuration key outside the search space");
+    if (err & 4)
+        return fail(TK_EINVAL, "load: an ok mean >= kFailFitness (1e10) would order above failed "
+                               "points (cache.hpp:15)");
+    if (err & 2) return fail(TK_EINVAL, "load: duplicate configuration key");
+    l->loaded = true;
+    return TK_OK;
+}
+
+// Build the open-addressing table of the loaded table's ok ranks (lazily, on
+// the first tk_land_lookup after a load).
+int ensure_hash(tk_land* l) {
+    if (l->hcap) return TK_OK;
+    Small* ds = l->small.as<Small>();
+    TKC(tk::launch_count_ok(l->ok.as<uint8_t>(), static_cast<uint32_t>(l->n), &ds->totals[0],
+                            l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->totals[0], &ds->totals[0], 8, cudaMemcpyDeviceToHost,
+                        l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    const uint64_t nv = l->hsmall->totals[0];
     uint64_t cap = 64;
     while (cap < 2 * nv) cap <<= 1;
     TKC(ensure(l->hkeys, cap * 8));
     TKC(ensure(l->hvals, cap * 8));
-    TKC(ensure(l->fit, (l->n + kPad) * 8));
-    TKC(ensure(l->ok, l->n + kPad));
-    l->hcap = cap;
-    Small* ds = l->small.as<Small>();
-    TKC(cudaMemsetAsync(l->hkeys.p, 0xFF, cap * 8, l->stream));
     TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
-    TKC(tk::launch_hash_build(dkeys, dvals, nv, l->n, l->hkeys.as<unsigned long long>(),
-                              l->hvals.as<double>(), cap, &ds->err, l->stream));
-    TKC(tk::launch_hash_densify(l->hkeys.as<unsigned long long>(), l->hvals.as<double>(), cap,
-                                static_cast<uint32_t>(l->n), l->fit.as<double>(),
-                                l->ok.as<uint8_t>(), l->stream));
+    TKC(tk::launch_hash_build(l->fit.as<double>(), l->ok.as<uint8_t>(), static_cast<uint32_t>(l->n),
+                              l->hkeys.as<unsigned long long>(), l->hvals.as<double>(), cap,
+                              &ds->err, l->stream));
     TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
-    l->built = l->pr_done = false;
-    if (l->hsmall->err == 1) {
-        l->loaded = false;
-        return fail(TK_EINVAL, "load: configuration key outside the search space");
-    }
-    if (l->hsmall->err == 2) {
-        l->loaded = false;
-        return fail(TK_EINVAL, "load: duplicate configuration key");
-    }
-    l->loaded = true;
-    l->opt_ready = false;
+    if (l->hsmall->err) return fail(TK_ECUDA, "valid-set hash table: probe bound exceeded");
+    l->hcap = cap;
     return TK_OK;
 }
 
@@ -693,7 +715,7 @@ int tk_land_destroy(tk_land* l) {
     cudaSetDevice(l->device);
     if (l->stream) cudaStreamSynchronize(l->stream);
     for (void* p : l->ipc_opened) cudaIpcCloseMemHandle(p);
-    DevBuf* bufs[] = {&l->fit, &l->ok, &l->hkeys, &l->hvals, &l->staging_keys, &l->staging_vals,
+    DevBuf* bufs[] = {&l->fit, &l->ok, &l->claimed, &l->hkeys, &l->hvals, &l->staging_keys, &l->staging_vals,
                       &l->staging_cfg, &l->pw, &l->inm, &l->odeg, &l->flags, &l->offsets,
                       &l->targets, &l->minima, &l->e_status, &l->m_status, &l->counter,
                       &l->om, &l->tile_cnt, &l->tile_base,
@@ -736,10 +758,19 @@ int tk_land_load_dense(tk_land* l, const double* fitness, const uint8_t* ok, int
     TKC(ensure(l->ok, l->n + kPad));
     TKC(cudaMemcpyAsync(l->fit.p, fitness, l->n * 8, h2x(mem), l->stream));
     TKC(cudaMemcpyAsync(l->ok.p, ok, l->n, h2x(mem), l->stream));
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
+    TKC(tk::launch_normalize_dense(static_cast<uint32_t>(l->n), l->fit.as<double>(),
+                                   l->ok.as<uint8_t>(), &ds->err, l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
-    l->loaded = true;
+    l->hcap = 0;
     l->opt_ready = false;
     l->built = l->pr_done = false;
+    l->loaded = !(l->hsmall->err & 4);
+    if (!l->loaded)
+        return fail(TK_EINVAL, "load_dense: an ok mean >= kFailFitness (1e10) would order above "
+                               "failed points (cache.hpp:15)");
     return TK_OK;
 }
 
@@ -809,6 +840,7 @@ int tk_land_generate(tk_land* l, int gen, double fail_fraction, uint64_t seed) {
     TKC(tk::launch_generate(gen, static_cast<uint32_t>(l->n), fail_fraction, seed,
                             l->fit.as<double>(), l->ok.as<uint8_t>(), l->stream));
     TKC(cudaStreamSynchronize(l->stream));
+    l->hcap = 0;
     l->loaded = true;
     l->opt_ready = false;
     l->built = l->pr_done = false;
@@ -829,18 +861,25 @@ int tk_land_copy_fitness(tk_land* l, double* fitness, uint8_t* ok) {
 int tk_land_lookup(tk_land* l, const uint64_t* keys, uint64_t n, double* fitness,
                    uint8_t* found) {
     if (int st = check_land(l)) return st;
-    if (!l->hcap) return fail(TK_ESTATE, "lookup: no hash table (load_sparse first)");
+    if (!l->loaded) return fail(TK_ESTATE, "lookup: nothing loaded");
+    if (n && !keys) return fail(TK_EINVAL, "lookup: null keys");
     TKC(set_dev(l));
+    if (int st = ensure_hash(l)) return st;
+    if (n == 0) return TK_OK;
     TKC(ensure(l->tmp, n * 17 + 16));
     unsigned long long* dq = l->tmp.as<unsigned long long>();
     double* dout = reinterpret_cast<double*>(dq + n);
     uint8_t* dfound = reinterpret_cast<uint8_t*>(dout + n);
+    Small* ds = l->small.as<Small>();
+    TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
     TKC(cudaMemcpyAsync(dq, keys, n * 8, cudaMemcpyHostToDevice, l->stream));
     TKC(tk::launch_hash_lookup(l->hkeys.as<unsigned long long>(), l->hvals.as<double>(), l->hcap,
-                               dq, n, dout, dfound, l->stream));
+                               dq, n, dout, dfound, &ds->err, l->stream));
     if (fitness) TKC(cudaMemcpyAsync(fitness, dout, n * 8, cudaMemcpyDeviceToHost, l->stream));
     if (found) TKC(cudaMemcpyAsync(found, dfound, n, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
+    if (l->hsmall->err) return fail(TK_ECUDA, "valid-set hash table: probe bound exceeded");
     return TK_OK;
 }
 

@@ -45,16 +45,24 @@ __device__ __forceinline__ double hash_uniform(unsigned long long seed, unsigned
 
 constexpr unsigned long long kEmpty = ~0ull;
 
-// Locality-preserving open-addressing slot: 32 consecutive keys share one
-// hashed 32-slot run, so a warp probing consecutive ranks reads one
-// contiguous 256 B segment of keys; runs are scattered by mix64.  A key whose
-// slot is taken probes the same position of the next runs (stride 32), so a
-// group displaced by another group moves to the next run together instead of
-// walking slot by slot through the occupied run (C5 valid set, unordered
-// keys: 17 -> ~2 atomic probes per key).
-__device__ __forceinline__ unsigned long long hslot(unsigned long long key,
-                                                   unsigned long long mask) {
-    return ((mix64(key >> 5) << 5) | (key & 31ull)) & mask;
+// Open-addressing probe sequence of the valid-set hash table (tk_land_lookup).
+// Probes 0..3 keep the locality-preserving pattern: 32 consecutive keys share
+// one hashed 32-slot run, so a warp probing consecutive ranks reads one
+// contiguous 256 B segment of keys, and a taken slot moves to the same
+// position of the next run, so a displaced group moves together.  Those
+// probes never leave the key's residue class mod 32, and constraint-shaped
+// valid sets (trailing parameters fixed, keys = 0 mod 4 or mod 32) fill a
+// class long before the table is full -- so from probe 4 on the sequence is
+// double hashing over the whole table: h1 + j*h2 with h2 odd and the capacity
+// a power of two visits every slot once in cap probes.  The table is sized to
+// >= 2x its keys, so build and lookup always meet an empty slot; kProbeCap
+// only guards the loops against a corrupted table (error flag, no spin).
+__device__ __forceinline__ unsigned long long hprobe(unsigned long long key, unsigned long long j,
+                                                    unsigned long long mask) {
+    if (j < 4) return (((mix64(key >> 5) + j) << 5) | (key & 31ull)) & mask;
+    const unsigned long long h1 = mix64(key ^ 0x6a09e667f3bcc909ULL);
+    const unsigned long long h2 = mix64(key + 0xbb67ae8584caa73bULL) | 1ull;
+    return (h1 + (j - 4) * h2) & mask;
 }
 
 template <typename T>
@@ -109,69 +117,109 @@ __global__ void encode_kernel(const int32_t* __restrict__ cfg, uint64_t nv, Enco
     }
 }
 
-__global__ void hash_build_kernel(const unsigned long long* __restrict__ keys,
-                                  const double* __restrict__ vals, uint64_t nv,
-                                  uint64_t n_nodes, unsigned long long* hkeys,
-                                  double* hvals, unsigned long long mask, int* err) {
+// ---- valid set -> dense rank-indexed table (load_sparse / load_configs) ----
+// Keys are mixed-radix ranks < N (space.cpp:72-78), so the rank-indexed
+// table the FFG reads anyway is a perfect hash of the valid set: the load
+// fills every rank with the failed entry (cache.hpp:15) and scatters the
+// valid pairs straight into it.  A bitmap of N bits (L2-resident: 14 MB at
+// C5) claims each key with one atomicOr, which detects duplicates.
+
+__global__ void fill_failed_kernel(uint32_t n, double* __restrict__ fit) {
+    for (uint64_t u = grid_stride_begin<uint64_t>(); u < n;
+         u += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        fit[u] = kFailFitness;
+}
+
+// err bits: 1 key outside the space, 2 duplicate key, 4 mean >= kFailFitness
+// (decision A11: an ok mean must order below every failed point)
+__global__ void valid_scatter_kernel(const unsigned long long* __restrict__ keys,
+                                     const double* __restrict__ vals, uint64_t nv, uint64_t n,
+                                     double* __restrict__ fit, uint8_t* __restrict__ ok,
+                                     unsigned int* __restrict__ claimed, int* err) {
     for (uint64_t i = grid_stride_begin<uint64_t>(); i < nv;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const unsigned long long k = keys[i];
-        if (k >= n_nodes) {
-            atomicExch(err, 1);
+        const double v = vals[i];
+        if (k >= n) {
+            atomicOr(err, 1);
             continue;
         }
-        unsigned long long s = hslot(k, mask);
-        while (true) {
-            const unsigned long long prev = atomicCAS(hkeys + s, kEmpty, k);
-            if (prev == kEmpty) {
-                hvals[s] = vals[i];
-                break;
-            }
-            if (prev == k) {
-                atomicExch(err, 2);
-                break;
-            }
-            s = (s + 32) & mask;  // next run, same lane position
+        if (v >= kFailFitness) atomicOr(err, 4);
+        const unsigned int bit = 1u << (k & 31);
+        const unsigned int old = atomicOr(claimed + (k >> 5), bit);
+        if (old & bit) {
+            atomicOr(err, 2);
+            continue;
         }
+        fit[k] = v;
+        ok[k] = 1;
     }
 }
 
-__global__ void hash_densify_kernel(const unsigned long long* __restrict__ hkeys,
-                                    const double* __restrict__ hvals,
-                                    unsigned long long mask, uint32_t n,
-                                    double* __restrict__ fit, uint8_t* __restrict__ ok) {
+// load_dense: failed entries are forced to kFailFitness (cache.cpp:49-53
+// set_failed) and an ok mean >= kFailFitness is rejected (A11).
+__global__ void normalize_dense_kernel(uint32_t n, double* __restrict__ fit,
+                                       const uint8_t* __restrict__ ok, int* err) {
+    bool bad = false;
     for (uint64_t u = grid_stride_begin<uint64_t>(); u < n;
          u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        unsigned long long s = hslot(u, mask);
-        double f = kFailFitness;
-        uint8_t good = 0;
-        while (true) {
-            const unsigned long long k = hkeys[s];
-            if (k == u) {
-                f = hvals[s];
-                good = 1;
+        const double f = fit[u];
+        if (ok[u]) bad |= f >= kFailFitness;
+        else if (!(f == kFailFitness)) fit[u] = kFailFitness;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 4);
+}
+
+__global__ void count_ok_kernel(const uint8_t* __restrict__ ok, uint32_t n,
+                                unsigned long long* count) {
+    unsigned int c = 0;
+    for (uint64_t u = grid_stride_begin<uint64_t>(); u < n;
+         u += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        c += ok[u] ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, static_cast<unsigned long long>(c));
+}
+
+// ---- open-addressing hash table of the valid set (tk_land_lookup) ----
+// Built from the dense table's ok ranks; every probe loop is bounded.
+constexpr unsigned long long kProbeCap = 1ull << 40;
+
+__global__ void hash_build_kernel(const double* __restrict__ fit, const uint8_t* __restrict__ ok,
+                                  uint32_t n, unsigned long long* hkeys, double* hvals,
+                                  unsigned long long mask, int* err) {
+    for (uint64_t u = grid_stride_begin<uint64_t>(); u < n;
+         u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (!ok[u]) continue;
+        const unsigned long long k = u;
+        const unsigned long long limit = 4 + mask + 1;
+        unsigned long long j = 0;
+        for (; j < limit && j < kProbeCap; ++j) {
+            const unsigned long long s = hprobe(k, j, mask);
+            const unsigned long long prev = atomicCAS(hkeys + s, kEmpty, k);
+            if (prev == kEmpty) {
+                hvals[s] = fit[u];
                 break;
             }
-            if (k == kEmpty) break;
-            s = (s + 32) & mask;  // next run, same lane position
         }
-        fit[u] = f;
-        ok[u] = good;
+        if (j == limit) atomicOr(err, 8);  // table full: cannot happen at cap >= 2 * keys
     }
 }
 
 __global__ void hash_lookup_kernel(const unsigned long long* __restrict__ hkeys,
                                    const double* __restrict__ hvals, unsigned long long mask,
                                    const unsigned long long* __restrict__ q, uint64_t nq,
-                                   double* __restrict__ out, uint8_t* __restrict__ found) {
+                                   double* __restrict__ out, uint8_t* __restrict__ found,
+                                   int* err) {
     for (uint64_t i = grid_stride_begin<uint64_t>(); i < nq;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const unsigned long long key = q[i];
-        unsigned long long s = hslot(key, mask);
         double f = kFailFitness;
         uint8_t hit = 0;
         if (key != kEmpty) {
-            while (true) {
+            const unsigned long long limit = 4 + mask + 1;
+            unsigned long long j = 0;
+            for (; j < limit; ++j) {
+                const unsigned long long s = hprobe(key, j, mask);
                 const unsigned long long k = hkeys[s];
                 if (k == key) {
                     f = hvals[s];
@@ -179,8 +227,8 @@ __global__ void hash_lookup_kernel(const unsigned long long* __restrict__ hkeys,
                     break;
                 }
                 if (k == kEmpty) break;
-                s = (s + 32) & mask;  // next run, same lane position
             }
+            if (j == limit) atomicOr(err, 8);
         }
         out[i] = f;
         found[i] = hit;
@@ -790,28 +838,49 @@ cudaError_t launch_encode_configs(const int32_t* configs, uint64_t n_valid, int 
     return cudaGetLastError();
 }
 
-cudaError_t launch_hash_build(const unsigned long long* keys, const double* vals,
-                              uint64_t n_valid, uint64_t n_nodes, unsigned long long* hkeys,
-                              double* hvals, uint64_t cap, int* err_flag,
-                              cudaStream_t stream) {
-    hash_build_kernel<<<grid_for(n_valid, 256, 148 * 16), 256, 0, stream>>>(
-        keys, vals, n_valid, n_nodes, hkeys, hvals, cap - 1, err_flag);
+cudaError_t launch_load_valid(const unsigned long long* keys, const double* vals,
+                              uint64_t n_valid, uint32_t n, double* fit, uint8_t* ok,
+                              unsigned int* claimed, int* err_flag, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(ok, 0, n, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(claimed, 0, ((n + 31ull) / 32) * 4, stream);
+    if (e != cudaSuccess) return e;
+    fill_failed_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(n, fit);
+    if (n_valid)
+        valid_scatter_kernel<<<grid_for(n_valid, 256, 148 * 16), 256, 0, stream>>>(
+            keys, vals, n_valid, n, fit, ok, claimed, err_flag);
     return cudaGetLastError();
 }
 
-cudaError_t launch_hash_densify(const unsigned long long* hkeys, const double* hvals,
-                                uint64_t cap, uint32_t n, double* fit, uint8_t* ok,
-                                cudaStream_t stream) {
-    hash_densify_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(hkeys, hvals, cap - 1,
-                                                                       n, fit, ok);
+cudaError_t launch_normalize_dense(uint32_t n, double* fit, const uint8_t* ok, int* err_flag,
+                                   cudaStream_t stream) {
+    normalize_dense_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(n, fit, ok, err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_ok(const uint8_t* ok, uint32_t n, unsigned long long* count,
+                            cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(count, 0, 8, stream);
+    if (e != cudaSuccess) return e;
+    count_ok_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, stream>>>(ok, n, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hash_build(const double* fit, const uint8_t* ok, uint32_t n,
+                              unsigned long long* hkeys, double* hvals, uint64_t cap,
+                              int* err_flag, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(hkeys, 0xFF, cap * 8, stream);
+    if (e != cudaSuccess) return e;
+    hash_build_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(fit, ok, n, hkeys, hvals,
+                                                                     cap - 1, err_flag);
     return cudaGetLastError();
 }
 
 cudaError_t launch_hash_lookup(const unsigned long long* hkeys, const double* hvals,
                                uint64_t cap, const unsigned long long* q, uint64_t nq,
-                               double* out, uint8_t* found, cudaStream_t stream) {
+                               double* out, uint8_t* found, int* err_flag, cudaStream_t stream) {
     hash_lookup_kernel<<<grid_for(nq, 256, 148 * 16), 256, 0, stream>>>(hkeys, hvals, cap - 1,
-                                                                       q, nq, out, found);
+                                                                       q, nq, out, found,
+                                                                       err_flag);
     return cudaGetLastError();
 }
 

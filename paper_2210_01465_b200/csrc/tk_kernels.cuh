@@ -14,16 +14,25 @@ cudaError_t launch_encode_configs(const int32_t* configs, uint64_t n_valid, int 
                                   const unsigned long long* strides_in_host,
                                   unsigned long long* keys_out, int* err_flag,
                                   cudaStream_t stream);
-cudaError_t launch_hash_build(const unsigned long long* keys, const double* vals,
-                              uint64_t n_valid, uint64_t n_nodes,
+// valid (key, fitness) pairs -> dense rank-indexed table; err bits 1 key >= N,
+// 2 duplicate key, 4 mean >= kFailFitness.  claimed: ceil(n/32) u32 scratch.
+cudaError_t launch_load_valid(const unsigned long long* keys, const double* vals,
+                              uint64_t n_valid, uint32_t n, double* fit, uint8_t* ok,
+                              unsigned int* claimed, int* err_flag, cudaStream_t stream);
+// failed entries -> kFailFitness; err bit 4 if an ok mean >= kFailFitness
+cudaError_t launch_normalize_dense(uint32_t n, double* fit, const uint8_t* ok, int* err_flag,
+                                   cudaStream_t stream);
+cudaError_t launch_count_ok(const uint8_t* ok, uint32_t n, unsigned long long* count,
+                            cudaStream_t stream);
+// open-addressing table of the ok ranks (cap a power of two >= 2 * ok count);
+// err bit 8 if a probe loop hit its bound
+cudaError_t launch_hash_build(const double* fit, const uint8_t* ok, uint32_t n,
                               unsigned long long* hkeys, double* hvals, uint64_t cap,
                               int* err_flag, cudaStream_t stream);
-cudaError_t launch_hash_densify(const unsigned long long* hkeys, const double* hvals,
-                                uint64_t cap, uint32_t n, double* fit, uint8_t* ok,
-                                cudaStream_t stream);
 cudaError_t launch_hash_lookup(const unsigned long long* hkeys, const double* hvals,
                                uint64_t cap, const unsigned long long* q, uint64_t nq,
-                               double* out, uint8_t* found, cudaStream_t stream);
+                               double* out, uint8_t* found, int* err_flag,
+                               cudaStream_t stream);
 cudaError_t launch_optimum(const double* fit, const uint8_t* ok, uint32_t n,
                            double* part_f, unsigned long long* part_r, double* f_opt,
                            unsigned long long* rank, int* has, cudaStream_t stream);

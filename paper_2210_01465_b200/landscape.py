@@ -105,9 +105,12 @@ class SearchSpaceCache:
         return int(self.ok_.sum())
 
     def _opt(self):
-        with Landscape(self.radix) as land:
-            land.load_dense(self.mean_, self.ok_)
-            return land.optimum()
+        # the cache is immutable (cache.hpp:23-25): one device pass, memoised
+        if getattr(self, "_opt_memo", None) is None:
+            with Landscape(self.radix) as land:
+                land.load_dense(self.mean_, self.ok_)
+                self._opt_memo = land.optimum()
+        return self._opt_memo
 
     def optimum(self) -> float:
         """cache.cpp:89-93 (computed on the device)."""
@@ -298,6 +301,12 @@ class Landscape:
         mn = np.empty(max(1, self.n_minima), np.uint32)
         _check(self.L.tk_ffg_copy_out(self.h, _ptr(off), _ptr(tg), _ptr(sk), _ptr(mn)))
         return off, tg[: self.n_edges], sk, mn[: self.n_minima]
+
+    def minima(self) -> np.ndarray:
+        """FitnessFlowGraph::minima (landscape.hpp:37) alone, without the CSR."""
+        mn = np.empty(max(1, self.n_minima), np.uint32)
+        _check(self.L.tk_ffg_copy_out(self.h, None, None, None, _ptr(mn)))
+        return mn[: self.n_minima]
 
     def census(self, with_ranks: bool = True) -> PointCensus:
         fp, lm, it = C.c_uint64(), C.c_uint64(), C.c_uint64()
@@ -620,9 +629,11 @@ def minima_fraction_report(cache: SearchSpaceCache, kind: int) -> MinimaFraction
         land.load_dense(cache.mean_, cache.ok_)
         land.build_ffg(kind, node_limit=1 << 32, emit_csr=False)
         f_opt, _ = land.optimum()
-        land.pagerank()  # report rows need a rank vector; cheap next to the FFG
-        _, _, frac, _ = land.report_rows(f_opt)
-    fr = np.sort(frac)
-    if fr.size == 0:
+        mins = land.minima()
+    fr = np.sort(f_opt / cache.mean_[mins])
+    k = fr.size
+    if k == 0:
         return MinimaFractionReport(fr)
-    return MinimaFractionReport(fr, float(np.median(fr)), float(fr.mean()))
+    med = fr[k // 2] if k % 2 else 0.5 * (fr[k // 2 - 1] + fr[k // 2])
+    # sequential sum (cumsum), the order of the C++ drop-in's loop
+    return MinimaFractionReport(fr, float(med), float(np.cumsum(fr)[-1] / k))
