@@ -1,7 +1,7 @@
 """bench.py -- FFG + PageRank GTEPS on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload c5|c3] [--kind adjacent|hamming]
+                    [--workload c5|c3|c4] [--kind adjacent|hamming]
 
 One step = analyze_landscape on one synthetic search space through the C-ABI:
 FFG build (CSR rows emitted, bit-exact), f_opt, PageRank to tol 1e-10 and
@@ -12,12 +12,18 @@ inside the timed region, minima report D2H after it).
 GTEPS = E * (iterations + 1) / t_step / 1e9: the FFG build traverses every
 edge once and each PageRank iteration once more.
 
-Multi-GPU (torchrun, one process per GPU): the one space is key-range
-sharded, one shard per GPU (paper_2210_01465_b200/sharded.py): each PageRank
-iteration pushes the contributions a peer pulls into that peer's replica over
-NVLink from inside the step kernel, and the per-shard partial sums are
-all-reduced with NCCL.  Total work is fixed ("scaling": "strong"); time is the
-max over ranks.
+Multi-GPU: `--gpus N` (N > 1) relaunches itself under torch.distributed.run
+(one process per GPU) unless it already runs under it.  The one space is
+key-range sharded, one shard per GPU (paper_2210_01465_b200/sharded.py): each
+PageRank iteration pushes the contributions a peer pulls into that peer's
+replica over NVLink from inside the step kernel, and the per-shard partial
+sums are all-reduced with NCCL.  Total work is one fixed space at every N
+("scaling": "strong"); time is the max over ranks.
+
+--impl reference: the CPU path (oracle/oracle.c, the C restatement of the
+reference's FFG / PageRank / C_p contract -- the reference declares the path
+but has no implementation) on the SAME workload: full space,
+PageRank to convergence, all host threads; plus a 1-thread column.
 """
 from __future__ import annotations
 
@@ -37,6 +43,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
+    # BASELINE.json configs[0]: 4-parameter GEMM-like, random table
+    "c1": dict(radix=(12, 12, 12, 12), gen=0, q=0.0, seed=1,
+               desc="synthetic 4-parameter GEMM-like space, 20,736 configs, random fitness "
+                    "table G_iid seed 1"),
+    # configs[1] (C2): 8-parameter conv-like, ~30 % invalid, the reference's own
+    # generate_synthetic_kernel_space "rugged" (host-generated: it uses libm sin)
+    "c2": dict(radix=(16, 12, 8, 8, 8, 4, 2, 2), gen=2, q=0.30, seed=2,
+               desc="synthetic 8-parameter convolution-like space, 1,572,864 configs (~1.1e6 "
+                    "valid, ~30 % failed), generate_synthetic_kernel_space 'rugged' seed 2"),
     # C5 "12-param ~1e8 valid", G_iid q = 0.10 seed 5
     "c5": dict(radix=(8, 8, 8, 6, 6, 6, 4, 4, 4, 4, 2, 2), gen=0, q=0.10, seed=5,
                desc="synthetic 12-parameter space, 113,246,208 configs (~1.02e8 valid), "
@@ -162,8 +177,9 @@ def run_batch(args, wl, kind):
             "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "parallelism": f"replicas{world}",
             "config": {"workload": "c4", "kind": args.kind, "desc": wl["desc"],
-                       "landscapes": n_lands, "parallelism": f"replicas{world}",
+                       "landscapes": n_lands,
                        "host_workers": workers,
                        "l2": "small landscapes; host upload per landscape inside the step"},
             "s_per_space": round(ms_step / 1e3 / n_lands, 7),
@@ -171,7 +187,7 @@ def run_batch(args, wl, kind):
             "roofline": None,
             "cpu_baseline": None,
             "e2e": {"value": round(edges / (t_ms / 1e3) / 1e9, 3), "unit": "GTEPS",
-                    "h2d_bytes_per_step": int(sum(9 * int(np.prod(it[1])) for it in items)),
+                    "h2d_bytes_per_step": int(sum(9 * int(np.prod(it[0])) for it in items)),
                     "d2h_bytes_per_step": int(sum(32 * s.n_minima for s in runs[-1]) * world),
                     "note": "the step itself is end to end: host upload + report per landscape "
                             "(tk.BatchAnalyzer: concurrent handles/streams)"},
@@ -182,22 +198,39 @@ def run_batch(args, wl, kind):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+FFG_BYTES_PER_NODE = 22
+FFG_BYTES_MODEL = ("22 B/node + 4 B/edge + 4 B/minimum: fitness 8 + ok 1 + packed word 4 + flags 1 "
+                   "+ CSR offset 8, targets, minima")
 KERNELS_PER_STEP = 8  # ffg_count, optimum_final, 2 slot scans, ffg_fill, pagerank, cp_partial, cp_final
 DAMPING, TOL, MAX_ITER, P_MAX = 0.85, 1e-10, 100000, 15
 
 
+def kernel_source_sha() -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in ("tk_staged.cu", "tk_internal.cuh"):
+        with open(os.path.join(ROOT, "paper_2210_01465_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def measured_traffic(workload: str, kind: str, iterations: int):
     """DRAM bytes (read + write) per PageRank launch from the committed ncu
-    --set full capture (profiles/r01_pagerank_traffic.json), when it was taken
-    on this workload; None otherwise."""
+    --set full capture (profiles/pagerank_traffic.json, scripts/
+    capture_traffic.sh), used only when it was taken on this workload AND on
+    this kernel source (sha of csrc/tk_staged.cu + tk_internal.cuh);
+    (None, why) otherwise."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_pagerank_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "pagerank_traffic.json")) as f:
             t = json.load(f)
     except (OSError, ValueError):
-        return None
+        return None, "no committed capture"
     if (t.get("workload"), t.get("kind"), t.get("iterations")) != (workload, kind, iterations):
-        return None
-    return t["dram_bytes_per_launch"]
+        return None, "capture taken on another workload"
+    if t.get("kernel_source_sha") != kernel_source_sha():
+        return None, f"capture taken on kernel source {t.get('kernel_source_sha')}, not this one"
+    return t["dram_bytes_per_launch"], t.get("source", "")
 
 
 def measured_peaks():
@@ -260,55 +293,123 @@ class ClockSampler:
 
 # --------------------------------------------------------------- CPU legs --
 
-def cpu_sample(wl: dict, kind: int, pr_iters: int = 3):
-    """Bounded CPU sample of the same workload: the first dim-0 slab of the
-    space (all other parameters intact), full FFG build with CSR and minima,
-    `pr_iters` PageRank iterations, C_p.  Oracle port, all host threads."""
+def host_cpu():
+    """nproc and the lscpu model name of this host."""
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
+
+
+def cpu_inputs(wl, radix=None, threads=None):
     import oracle as O
 
-    radix = list(wl["radix"])
-    radix[0] = 1
-    n = O.space_size(radix)
-    threads = os.cpu_count() or 1
+    radix = list(radix or wl["radix"])
+    nt = threads or os.cpu_count() or 1
+    if wl["gen"] == 2:
+        return radix, *O.gen_synthetic(radix, wl["q"], "rugged", wl["seed"], nthreads=nt)
     gen = O.gen_iid if wl["gen"] == 0 else O.gen_heavy
-    fit, ok = gen(n, wl["q"], wl["seed"], nthreads=threads)
+    return radix, *gen(O.space_size(radix), wl["q"], wl["seed"], nthreads=nt)
+
+
+def cpu_analyze(radix, fit, ok, kind, threads):
+    """One analyze_landscape on the CPU path (oracle/oracle.c): FFG build with
+    CSR and minima, f_opt, PageRank to convergence (tol 1e-10; the out-CSR is
+    transposed inside, as pagerank(const FitnessFlowGraph&) must), C_p for
+    p = 0..15 %.  Per-phase wall times."""
+    import oracle as O
+
     t0 = time.perf_counter()
     g = O.build_ffg(radix, fit, ok, kind, node_limit=1 << 32, nthreads=threads)
-    pr, it, _ = O.pagerank(g["offsets"], g["targets"], DAMPING, TOL, MAX_ITER,
-                           nthreads=threads, fixed_iters=pr_iters)
+    t1 = time.perf_counter()
     f_opt, _ = O.optimum(fit, ok)
-    for k in range(P_MAX + 1):
-        O.proportion_of_centrality(g["minima"], fit, pr, f_opt, k / 100.0)
-    dt = time.perf_counter() - t0
+    pr, it, _ = O.pagerank(g["offsets"], g["targets"], DAMPING, TOL, MAX_ITER, nthreads=threads)
+    t2 = time.perf_counter()
+    curve = [O.proportion_of_centrality(g["minima"], fit, pr, f_opt, k / 100.0)
+             for k in range(P_MAX + 1)]
+    t3 = time.perf_counter()
     e = len(g["targets"])
-    return dict(value=e * (pr_iters + 1) / dt / 1e9, seconds=dt, edges=e, nodes=n,
-                threads=threads, iters=pr_iters)
+    return dict(value=e * (it + 1) / (t3 - t0) / 1e9, seconds=t3 - t0, edges=e,
+                nodes=len(fit), minima=g["minima"], iterations=it, pagerank=pr, c_p=curve,
+                threads=threads,
+                phases_s={"ffg": round(t1 - t0, 3), "pagerank": round(t2 - t1, 3),
+                          "centrality": round(t3 - t2, 3)})
+
+
+def cpu_one_thread(wl, kind):
+    """The 1-thread column (the reference code has no threads) on
+    a bounded sample: the first dim-0 slab of the workload (every other
+    parameter intact), full analysis to convergence."""
+    radix = list(wl["radix"])
+    radix[0] = 1
+    radix, fit, ok = cpu_inputs(wl, radix)
+    c = cpu_analyze(radix, fit, ok, kind, 1)
+    return {"value": round(c["value"], 5), "unit": "GTEPS", "cores": 1,
+            "sample": f"first dim-0 slab ({c['nodes']} configs, {c['edges']} edges, "
+                      f"{c['iterations']} PageRank iterations to convergence), {c['seconds']:.1f} s",
+            "phases_s": c["phases_s"]}
+
+
+def config_block(args, wl, n, e, m, iters):
+    """The `config` object, identical in both arms for one workload."""
+    return {"workload": args.workload, "kind": args.kind, "desc": wl["desc"], "nodes": n,
+            "edges": e, "minima": m, "pagerank_iterations": iters, "damping": DAMPING,
+            "tol": TOL, "l2": l2_note(n, e)}
+
+
+def l2_note(n, e):
+    state = 9 * n + 4 * e + 8 * n + 32 * n  # table, CSR targets + offsets, PageRank vectors
+    if state > 126e6:
+        return (f"inputs larger than L2 ({9 * n / 1e9:.2f} GB fitness table, "
+                f"~{state / 1e9:.1f} GB FFG/PageRank state vs 126 MB L2)")
+    return (f"inputs smaller than L2 (~{state / 1e6:.1f} MB state): steps run back to back "
+            "without an L2 flush (a parity/latency workload, not the headline line)")
 
 
 def run_reference(args, wl, kind):
+    """The reference arm: the CPU path on the same workload as the GPU arm
+    (whole space, PageRank to convergence, C_p curve), all host threads.  The
+    input table is generated once, outside the timed steps (as the GPU arm's
+    `value` has it resident)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    threads = os.cpu_count() or 1
+    radix, fit, ok = cpu_inputs(wl)
     for _ in range(args.warmup):
-        cpu_sample(wl, kind)
-    vals, secs = [], 0.0
-    for _ in range(args.steps):
-        s = cpu_sample(wl, kind)
-        vals.append(s["value"])
-        secs += s["seconds"]
-    v = float(np.mean(vals))
-    sample = (f"first dim-0 slab of {args.workload} ({s['nodes']} configs, {s['edges']} edges): "
-              f"FFG build + {s['iters']} PageRank iterations + C_p per step")
+        cpu_analyze(radix, fit, ok, kind, threads)
+    runs = [cpu_analyze(radix, fit, ok, kind, threads) for _ in range(args.steps)]
+    secs = sum(r["seconds"] for r in runs)
+    last = runs[-1]
+    edges = sum(r["edges"] * (r["iterations"] + 1) for r in runs)
+    v = edges / secs / 1e9
+    one = cpu_one_thread(wl, kind)
+    host = host_cpu()
     line = {
-        "metric": "FFG+PageRank GTEPS", "value": v, "unit": "GTEPS", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"]},
-        "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": s["threads"], "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+        "metric": "FFG+PageRank GTEPS", "value": round(v, 5), "unit": "GTEPS",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args, wl, last["nodes"], last["edges"], len(last["minima"]),
+                               last["iterations"]),
+        "phases_s": last["phases_s"],
+        "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": threads,
+                         "kind": "port", "host": host, "same_config": True,
+                         "sample": f"the whole {args.workload} workload per step ({last['nodes']} "
+                                   f"configs, {last['edges']} edges, {last['iterations']} "
+                                   f"PageRank iterations): oracle/oracle.c, OpenMP, {threads} "
+                                   "threads",
+                         "one_thread": one},
+        "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reproduce": f"python bench.py --impl reference --workload {args.workload} "
+                     f"--kind {args.kind} --steps {args.steps} --warmup {args.warmup}",
     }
     print(json.dumps(line))
     return 0
@@ -332,7 +433,12 @@ def run_b200(args, wl, kind):
 
     radix = wl["radix"]
     land = tk.Landscape(radix, device=local)
-    land.generate(wl["gen"], wl["q"], wl["seed"] + 0)  # identical replica on every rank
+    if wl["gen"] == 2:  # the reference's generator, host-side (libm sin), then uploaded
+        hfit, hok = host_generator()(radix, wl["q"], wl["seed"])
+        land.load_dense(hfit, hok)
+        del hfit, hok
+    else:
+        land.generate(wl["gen"], wl["q"], wl["seed"])  # device generator, bit-identical
     stream = torch.cuda.ExternalStream(land.stream, device=torch.device("cuda", local))
 
     def step():
@@ -377,6 +483,45 @@ def run_b200(args, wl, kind):
 
     n = land.n
     kinfo = land.kernel_info()
+    e_last, m_last, it_last = sums[-1].n_edges, sums[-1].n_minima, sums[-1].iterations
+
+    # ---- the GPU results of this workload, kept for the parity check below
+    gpu_minima = gpu_pr = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gpu_minima = land.minima().astype(np.int64)
+        gpu_pr = land.pagerank_vector()
+    gpu_curve = list(sums[-1].c_p[: sums[-1].n_cp])
+
+    # ---- second column: the same space under the Hamming neighbourhood
+    ham = None
+    if args.kind == "adjacent" and not args.no_hamming:
+        hs = [land.analyze(0, DAMPING, TOL, MAX_ITER, node_limit=1 << 32,
+                           p_max_percent=P_MAX, emit_csr=True)]  # warm
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        hs = [land.analyze(0, DAMPING, TOL, MAX_ITER, node_limit=1 << 32, p_max_percent=P_MAX,
+                           emit_csr=True) for _ in range(3)]
+        h1.record(stream)
+        h1.synchronize()
+        h_ms = h0.elapsed_time(h1) / 3
+        he, hit = hs[-1].n_edges, hs[-1].iterations
+        hpr = float(np.mean([x.ms_pagerank for x in hs]))
+        # contribution-only Hamming iteration: u64 in-mask 8 + outdeg 1 + c read once 8 + c' 8
+        hbytes = 25 * n * hit + 33 * n
+        peaks, _ = measured_peaks()
+        ham = {"value": round(he * (hit + 1) * 3 / (h_ms * 3 / 1e3) / 1e9, 3), "unit": "GTEPS",
+               "ms_per_step": round(h_ms, 3), "edges": he, "pagerank_iterations": hit,
+               "phases_ms": {"ffg_build_kernel": round(float(np.mean([x.ms_ffg for x in hs])), 3),
+                             "pagerank_kernel": round(hpr, 3)},
+               "roofline": {"bound": "hbm", "kernel": "pagerank_ham_tiled_kernel",
+                            "achieved": round(hbytes / (hpr / 1e3) / 1e9, 1),
+                            "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": round(hbytes / (hpr / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                            "bytes_model": "25 B/node/iteration: u64 in-mask 8 + outdeg 1 + c "
+                                           "read once 8 + c' 8; + 33 B/node prologue and "
+                                           "closing pass",
+                            "algorithmic_bytes_per_launch": hbytes}}
 
     # ---- e2e: the same analysis from pinned host buffers through the public API.
     # tk.AnalysisPipeline double-buffers two device handles: every step uploads its
@@ -388,7 +533,7 @@ def run_b200(args, wl, kind):
     f_np, o_np = land.fitness()
     fit_h.numpy()[:] = f_np
     ok_h.numpy()[:] = o_np
-    m = sums[-1].n_minima
+    m = m_last
     land.close()  # free this handle's device state; the pipeline holds two of its own
     torch.cuda.synchronize(local)
     rep = [[torch.empty(m, dtype=torch.float64, pin_memory=True) for _ in range(4)]
@@ -411,7 +556,6 @@ def run_b200(args, wl, kind):
 
     # ---- roofline of the dominant kernel (persistent PageRank, one launch per step)
     peaks, peak_src = measured_peaks()
-    it_last = sums[-1].iterations
     if land_mode_packed(radix, kind):
         # contribution-only iteration: packed word 4 + c read once 8 + c' 8;
         # prologue writes c_0 (pw 4 + 8), the closing pass materialises r' (pw 4 + c 8 + r 8)
@@ -425,43 +569,67 @@ def run_b200(args, wl, kind):
     pr_bytes = per_pro + per_iter * it_last
     achieved = pr_bytes / (pr_ms / 1e3) / 1e9
     ffg_ms = float(np.mean([x.ms_ffg for x in sums]))
+    traffic, traffic_src = measured_traffic(args.workload, args.kind, it_last)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                "traffic": measured_traffic(args.workload, args.kind, it_last),
+                "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "pagerank_staged_kernel (persistent, cooperative)",
                 "bytes_model": model, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pr_bytes, "kernel_ms": round(pr_ms, 3),
                 "iterations": it_last, "kernels": kinfo}
+    ffg_bytes = FFG_BYTES_PER_NODE * n + 4 * e_last + 4 * m_last
+    roofline_ffg = {"bound": "hbm", "kernel": "ffg_count_staged_kernel + ffg_fill_kernel",
+                    "achieved": round(ffg_bytes / (ffg_ms / 1e3) / 1e9, 1),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(ffg_bytes / (ffg_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                    "bytes_model": FFG_BYTES_MODEL, "algorithmic_bytes_per_build": ffg_bytes,
+                    "phase_ms": round(ffg_ms, 3)}
 
     out = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            c = cpu_sample(wl, kind)
-            cpu = {"value": round(c["value"], 4), "unit": "GTEPS", "cores": c["threads"],
-                   "kind": "port",
-                   "sample": f"oracle/oracle.c (OpenMP) on the first dim-0 slab of "
-                             f"{args.workload}: {c['nodes']} configs, {c['edges']} edges, FFG "
-                             f"+ {c['iters']} PageRank iterations + C_p, {c['seconds']:.1f} s"}
-        ffg_bytes = 22 * n + 4 * e + 4 * sums[-1].n_minima
+            threads = os.cpu_count() or 1
+            _, cfit, cok = cpu_inputs(wl)
+            c = cpu_analyze(list(radix), cfit, cok, kind, threads)
+            # parity of this very run: the GPU results above against the CPU path
+            parity = {
+                "edges_equal": c["edges"] == e_last,
+                "minima_equal": bool(np.array_equal(c["minima"].astype(np.int64), gpu_minima)),
+                "iterations_equal": c["iterations"] == it_last,
+                "pagerank_rel_l1": float(np.abs(gpu_pr - c["pagerank"]).sum()
+                                         / np.abs(c["pagerank"]).sum()),
+                "c_p_max_abs_diff": float(max(abs(a - b) for a, b in zip(gpu_curve, c["c_p"]))),
+            }
+            parity["ok"] = bool(parity["edges_equal"] and parity["minima_equal"]
+                                and parity["iterations_equal"]
+                                and parity["pagerank_rel_l1"] <= 1e-12
+                                and parity["c_p_max_abs_diff"] <= 1e-9)
+            cpu = {"value": round(c["value"], 5), "unit": "GTEPS", "cores": threads,
+                   "kind": "port", "host": host_cpu(), "same_config": True,
+                   "sample": f"the whole {args.workload} workload once ({c['nodes']} configs, "
+                             f"{c['edges']} edges, {c['iterations']} PageRank iterations): "
+                             f"oracle/oracle.c, OpenMP, {threads} threads, {c['seconds']:.1f} s",
+                   "phases_s": c["phases_s"],
+                   "one_thread": cpu_one_thread(wl, kind),
+                   "parity_vs_gpu": parity}
+            del c
         out = {
             "metric": "FFG+PageRank GTEPS", "value": round(value, 3), "unit": "GTEPS",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"],
-                       "nodes": n, "edges": e, "minima": sums[-1].n_minima,
-                       "pagerank_iterations": it_last, "damping": DAMPING, "tol": TOL,
-                       "parallelism": f"replicas{world}",
-                       "l2": "inputs larger than L2 (1.0 GB fitness, ~11 GB FFG/PageRank state)"},
+            "parallelism": f"replicas{world}",
+            "config": config_block(args, wl, n, e_last, m_last, it_last),
             "s_per_space": round(ms_step / 1e3, 5),
             "phases_ms": {"ffg_build_kernel": round(ffg_ms, 3),
                           "pagerank_kernel": round(pr_ms, 3),
                           "centrality": round(float(np.mean([x.ms_centrality for x in sums])), 3)},
-            "ffg_edges_per_s": round(e / (ffg_ms / 1e3), 1),
-            "ffg_build_gbs": round(ffg_bytes / (ffg_ms / 1e3) / 1e9, 1),
-            "pagerank_gteps": round(e * it_last / (pr_ms / 1e3) / 1e9, 3),
+            "ffg_edges_per_s": round(e_last / (ffg_ms / 1e3), 1),
+            "pagerank_gteps": round(e_last * it_last / (pr_ms / 1e3) / 1e9, 3),
             "roofline": roofline,
+            "roofline_ffg": roofline_ffg,
+            "hamming": ham,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GTEPS",
                     "h2d_bytes_per_step": 9 * n, "d2h_bytes_per_step": 32 * m,
@@ -503,7 +671,12 @@ def run_sharded(args, wl, kind):
 
     radix = wl["radix"]
     shard = S.GpuShard(radix, rank, world, device=local)
-    shard.land.generate(wl["gen"], wl["q"], wl["seed"])  # read-only table, replicated
+    if wl["gen"] == 2:
+        hfit, hok = host_generator()(radix, wl["q"], wl["seed"])
+        shard.land.load_dense(hfit, hok)
+        del hfit, hok
+    else:
+        shard.land.generate(wl["gen"], wl["q"], wl["seed"])  # read-only table, replicated
     allreduce, allgather = S.torch_collectives(device=f"cuda:{local}")
     S.connect_peers_ipc(shard, allgather)
     stream = torch.cuda.ExternalStream(shard.land.stream, device=torch.device("cuda", local))
@@ -583,11 +756,10 @@ def run_sharded(args, wl, kind):
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "kind": args.kind, "desc": wl["desc"],
-                       "nodes": n, "edges": e, "minima": runs[-1]["n_minima"],
-                       "pagerank_iterations": it, "parallelism": f"keyrange{world}",
-                       "shard_push": os.environ.get("TK_SHARD_PUSH", "crossing"),
-                       "l2": "inputs larger than L2"},
+            "parallelism": f"keyrange{world}", "dist_backend": backend,
+            "shard_push": os.environ.get("TK_SHARD_PUSH", "crossing"),
+            "nvlink_bytes_per_gpu_per_iteration": nvlink_push_bytes(radix, world),
+            "config": config_block(args, wl, n, e, runs[-1]["n_minima"], it),
             "s_per_space": round(ms_step / 1e3, 5),
             "roofline": {"bound": "hbm", "achieved": round(per_gpu_bytes / (ms_step / 1e3) / 1e9, 1),
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -610,6 +782,47 @@ def run_sharded(args, wl, kind):
     return 0
 
 
+def nvlink_push_bytes(radix, world: int) -> int:
+    """Expected NVLink bytes one GPU stores into its peers per PageRank
+    iteration under TK_SHARD_PUSH=crossing: c'[v] (8 B) along
+    every direction (dim i, +/-) whose neighbour exists and lies in another
+    shard, counted over the largest shard."""
+    from paper_2210_01465_b200.sharded import shard_range
+
+    radix = [m for m in radix if m >= 2]
+    n = int(np.prod(radix))
+    strides = [int(np.prod(radix[i + 1:])) for i in range(len(radix))]
+    worst = 0
+    for g in range(world):
+        lo, hi = shard_range(n, g, world)
+        tot = 0
+        for s_i, m_i in zip(strides, radix):
+            # + direction: v in [max(lo, hi - s_i), hi) with digit_i(v) < m_i - 1
+            v = np.arange(max(lo, hi - s_i), hi, dtype=np.int64)
+            tot += int(((v // s_i) % m_i < m_i - 1).sum()) if hi < n else 0
+            v = np.arange(lo, min(hi, lo + s_i), dtype=np.int64)
+            tot += int(((v // s_i) % m_i > 0).sum()) if lo > 0 else 0
+        worst = max(worst, 8 * tot)
+    return worst
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: run this same command
+    under torch.distributed.run, one process per GPU (rendezvous on
+    127.0.0.1).  Rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator size visible in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def land_mode_packed(radix, kind) -> bool:
     dims = sum(1 for m in radix if m >= 2)
     return kind == 1 and 2 * dims <= 27
@@ -624,7 +837,10 @@ def main() -> int:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5")
     ap.add_argument("--kind", choices=sorted(KIND), default="adjacent")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-hamming", action="store_true", help="skip the Hamming column")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     wl = WORKLOADS[args.workload]
     kind = KIND[args.kind]
     if args.impl == "reference":

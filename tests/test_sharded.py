@@ -254,20 +254,28 @@ def test_virtual_gpu_shards_match_oracle(radix, nshards, push, monkeypatch):
         s.land.close()
 
 
-def _gpu_ipc_worker(rank, world, port, out, dev_loop=False):
+def _gpu_ipc_worker(rank, world, port, out, dev_loop=False, backend="gloo"):
+    import torch
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0  # nccl: one GPU per rank, peers over NVLink
+    if backend == "nccl":
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         radix = [8, 8, 6, 6, 4, 4, 2]
         n = O.space_size(radix)
         fit, ok = O.gen_iid(n, 0.2, 31)
-        shard = S.GpuShard(radix, rank, world, device=0)
+        shard = S.GpuShard(radix, rank, world, device=dev)
         shard.land.load_dense(fit, ok)
-        allreduce, allgather = S.torch_collectives()
+        allreduce, allgather = S.torch_collectives(device=f"cuda:{dev}" if backend == "nccl"
+                                                   else None)
         S.connect_peers_ipc(shard, allgather)
-        loop = S.device_pagerank_loop(shard, "cuda:0") if dev_loop else None
+        loop = S.device_pagerank_loop(shard, f"cuda:{dev}") if dev_loop else None
         res = S.analyze_sharded([shard], allreduce, allgather, O.ADJACENT, pagerank_loop=loop)
         r = shard.land.shard_pagerank_vector(shard.lo, shard.hi)
         if loop is not None:
@@ -312,6 +320,67 @@ def test_two_processes_one_gpu_cuda_ipc(dev_loop):
     check(got[0][0], ref, fit, ok, O.ADJACENT)
     r = np.concatenate([got[k][2] for k in (0, 1)])
     assert np.abs(r - ref["pagerank"]).sum() <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_nccl_device_loop_multi_gpu(world):
+    """DevicePagerankLoop under NCCL, one process per GPU, peers' replicas
+    mapped over NVLink with CUDA IPC.  Needs `world` visible GPUs."""
+    import torch
+
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_ipc_worker, args=(r, world, port, q, True, "nccl"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        rk, res, lo, r = q.get(timeout=300)
+        got[rk] = (res, lo, r)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    radix = [8, 8, 6, 6, 4, 4, 2]
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, 0.2, 31)
+    ref = O.analyze(radix, fit, ok, O.ADJACENT, node_limit=1 << 32)
+    check(got[0][0], ref, fit, ok, O.ADJACENT)
+    r = np.concatenate([got[k][2] for k in range(world)])
+    assert np.abs(r - ref["pagerank"]).sum() <= 1e-12
+
+
+@pytest.mark.gpu
+def test_bench_self_launch_two_ranks_one_gpu():
+    """`python bench.py --gpus 2` with no launcher re-executes itself under
+    torch.distributed.run; on a one-GPU box both ranks share the device over
+    gloo (TK_FORCE_DEVICE=0).  Rank 0 prints one N=2 line."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TK_FORCE_DEVICE="0", TK_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--workload", "c3", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["parallelism"] == "keyrange2"
+    assert line["scaling"] == "strong" and line["value"] > 0
+    assert line["nvlink_bytes_per_gpu_per_iteration"] > 0
 
 
 @pytest.mark.parametrize("kind", [O.ADJACENT, O.HAMMING])
