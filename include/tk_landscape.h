@@ -87,8 +87,9 @@ int tk_land_reshape(tk_land* land, uint32_t dims, const uint32_t* radix);
 int tk_land_info(const tk_land* land, uint64_t* n_nodes, int* device);
 /* The cudaStream_t every kernel of this handle is launched on (for events). */
 void* tk_land_stream(tk_land* land);
-/* Which kernels the last build / PageRank used (1 = TMA-staged Adjacent path,
- * 0 = per-lane gathers), the PageRank grid size and the kernel-only device
+/* Which kernels the last build / PageRank used (build: 1 = TMA-staged Adjacent
+ * path, 0 = per-lane gathers; PageRank: 2 = row-tiled Adjacent kernel, 1 =
+ * TMA-staged, 0 = per-lane gathers), the PageRank grid size and the kernel-only device
  * times of the last build and PageRank launches (ms).  Any pointer may be NULL. */
 int tk_land_kernel_info(const tk_land* land, int* staged_build, int* staged_pagerank,
                         int* pagerank_grid, float* ms_build, float* ms_pagerank);

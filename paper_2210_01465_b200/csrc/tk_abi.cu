@@ -127,7 +127,7 @@ struct tk_land {
     cudaEvent_t ev[6] = {};
     float ms_build = 0.f, ms_pr = 0.f;  // kernel-only device time of the last launch
     bool staged = false;                // last build used the TMA-staged kernel
-    bool pr_staged = false;             // last PageRank used the TMA-staged kernel
+    int pr_staged = 0;                  // last PageRank kernel: 0 per-lane, 1 staged, 2 row-tiled
     int pr_grid = 0;
     bool opt_ready = false;  // small->f_opt/rank/has hold f_opt of the loaded table
 
@@ -426,8 +426,8 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                  tk::PrArgs a, DevBuf& part, Small* ds, Small* hs, cudaStream_t stream,
                  double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
                  cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr,
-                 const tk::StagePlan* plan = nullptr) {
-    const int maxg = plan ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
+                 const tk::StagePlan* plan = nullptr, const tk::RowPlan* rplan = nullptr) {
+    const int maxg = (plan || rplan) ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
     TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
     const double nd = static_cast<double>(a.n);
@@ -447,12 +447,14 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
     if (e0) TKC(cudaEventRecord(e0, stream));
     // SM footprint: the staged kernel runs one CTA per SM on min(SMs, tiles)
     // SMs; the per-lane kernel is sized to the whole device
-    const int footprint = plan ? static_cast<int>(std::min<uint64_t>(
+    const int footprint = rplan ? static_cast<int>(std::min<uint64_t>(num_sms, rplan->ncols))
+                          : plan ? static_cast<int>(std::min<uint64_t>(
                                      num_sms, (static_cast<uint64_t>(a.n) + plan->T - 1) / plan->T))
                                : num_sms;
     const bool ham_tiled = !plan && mode == tk::MODE_HAM && staged_enabled() &&
                            tk::ham_tiled_supported(s);
     TKC(gated_coop_launch(device, num_sms, ham_tiled ? num_sms : footprint, stream, [&] {
+        if (rplan) return tk::launch_pagerank_rows(s, *rplan, a, num_sms, &g, stream);
         if (plan) return tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream);
         if (ham_tiled) return tk::launch_pagerank_ham_tiled(s, wide, a, num_sms, &g, stream);
         return tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
@@ -485,13 +487,17 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     a.c0 = l->c0.as<double>();
     a.c1 = l->c1.as<double>();
     tk::StagePlan plan{};
-    const bool have_plan = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+    tk::RowPlan rplan{};
+    const bool have_rows = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+                           tk::make_row_plan(l->shape, l->num_sms, &rplan);
+    const bool have_plan = !have_rows && l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
                            tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false);
-    l->pr_staged = have_plan;
+    l->pr_staged = have_rows ? 2 : have_plan ? 1 : 0;
     l->pr_done = false;
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
                       l->small.as<Small>(), l->hsmall, l->stream, d, tol, max_iter, l->ev[2],
-                      l->ev[3], &l->ms_pr, &l->pr_grid, have_plan ? &plan : nullptr);
+                      l->ev[3], &l->ms_pr, &l->pr_grid, have_plan ? &plan : nullptr,
+                      have_rows ? &rplan : nullptr);
     if (st) return st;
     const PrOut& o = l->hsmall->pr;
     l->iterations = o.iter;
@@ -743,7 +749,7 @@ int tk_land_kernel_info(const tk_land* l, int* staged_build, int* staged_pageran
                         int* pagerank_grid, float* ms_build, float* ms_pagerank) {
     if (int st = check_land(l)) return st;
     if (staged_build) *staged_build = l->staged ? 1 : 0;
-    if (staged_pagerank) *staged_pagerank = l->pr_staged ? 1 : 0;
+    if (staged_pagerank) *staged_pagerank = l->pr_staged;
     if (pagerank_grid) *pagerank_grid = l->pr_grid;
     if (ms_build) *ms_build = l->ms_build;
     if (ms_pagerank) *ms_pagerank = l->ms_pr;

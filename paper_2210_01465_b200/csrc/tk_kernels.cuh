@@ -2,6 +2,8 @@
 // Every wrapper enqueues on `stream` and returns a cudaError_t; none blocks.
 #pragma once
 
+#include <cuda.h>
+
 #include "tk_internal.cuh"
 
 namespace tk {
@@ -209,6 +211,44 @@ cudaError_t launch_pagerank_shard_step(const DevShape& s, const StagePlan& p, co
 // r[v] over the shard's ranks [lo, hi) from its contributions c (shard_materialize_kernel)
 cudaError_t launch_shard_materialize(uint64_t lo, uint64_t hi, const uint32_t* pw, const double* c,
                                     double* r, int num_sms, cudaStream_t stream);
+
+// ---- row-tiled Adjacent PageRank (tk_rows.cu) --------------------------------
+// For spaces whose trailing dims span exactly 16 ranks (a "row") and N % 512 == 0.
+// Non-row dims split into far dims 0..nfar-1 (one staged 32-row range per
+// direction and tile) and window dims nfar..nfar+nwin-1 (served from a per-CTA
+// ring of the column's rows).  A column (super-column) is col_rows consecutive
+// rows, a whole number of 32-row tiles; columns are dealt round-robin to CTAs.
+struct RowPlan {
+    int dims;                   // effective dims (DevShape::dims)
+    int nrow_dims;              // trailing dims inside a row
+    int row_radix[4];           // their radices, most significant first
+    int nfar, nwin;             // far dims / window dims
+    int ahead;                  // A = ceil(largest window stride in rows / 32)
+    uint32_t rows;              // N / 16
+    uint32_t col_rows, ncols, tiles_per_col;
+    unsigned long long tpc_magic;                 // fdiv magic of tiles_per_col
+    int win_rows[kMaxDims];                       // row stride of window dim nfar + k
+    uint32_t far_rows[kMaxDims];                  // row stride of far dim d
+    uint32_t far_radix[kMaxDims];
+    unsigned long long far_magic[kMaxDims];       // fdiv magic of far_rows[d]
+    unsigned long long far_rmagic[kMaxDims];      // fdiv magic of far_radix[d]
+    int far_span[kMaxDims];                       // a 32-row tile spans several digits
+    uint32_t far_ef;                              // far dims loaded L2 evict-first (bit d)
+    int far_per_col;                              // columns are whole tiles: far digits per column
+};
+// TMA tensor maps of the rank-vector buffers viewed as [rows][16] f64 (SWIZZLE_128B)
+// and of the packed words as [rows][16] u32 (SWIZZLE_64B), 32-row boxes.
+// Loads use [rows][16] boxes; the consumer warps store half rows ([rows][8]
+// boxes, SWIZZLE_64B) of c' (cs) and of the closing r' pass (r0s).
+struct alignas(64) RowMaps {
+    CUtensorMap c[2];
+    CUtensorMap pw;
+    CUtensorMap cs[2];
+    CUtensorMap r0s;
+};
+bool make_row_plan(const DevShape& s, int num_sms, RowPlan* plan);
+cudaError_t launch_pagerank_rows(const DevShape& s, const RowPlan& p, const PrArgs& a,
+                                 int num_sms, int* grid_out, cudaStream_t stream);
 
 // ---- C_p and report -------------------------------------------------------
 constexpr int kCpBlocks = 148 * 8;  // enough warps to hide the dependent minima -> (f, r) gathers

@@ -235,7 +235,8 @@ class Landscape:
         mb, mp = C.c_float(), C.c_float()
         _check(self.L.tk_land_kernel_info(self.h, C.byref(sb), C.byref(sp), C.byref(g),
                                           C.byref(mb), C.byref(mp)))
-        return dict(staged_build=bool(sb.value), staged_pagerank=bool(sp.value),
+        return dict(staged_build=bool(sb.value), staged_pagerank=sp.value > 0,
+                    pagerank_kernel={2: "rows", 1: "staged"}.get(sp.value, "per-lane"),
                     pagerank_grid=g.value, ms_build=mb.value, ms_pagerank=mp.value)
 
     # ---- ingestion

@@ -29,7 +29,7 @@ fi
 if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"
   echo "exit=$?" >> "$OUT/bench.err"
-  /usr/bin/time -v timeout 1200 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 \
+  timeout 1200 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 \
       > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
   timeout 600 python bench.py --workload c4 --steps 2 > "$OUT/bench_c4.json" 2> "$OUT/bench_c4.err"
   # N=2 without a launcher: bench.py re-executes itself under torch.distributed.run;
@@ -37,6 +37,21 @@ if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   TK_FORCE_DEVICE=0 TK_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 2 \
       --warmup 3 > "$OUT/bench_shard2_c5.json" 2> "$OUT/bench_shard2_c5.err"
   echo "exit=$?" >> "$OUT/bench_shard2_c5.err"
+fi
+
+if [[ $WHAT == all || $WHAT == hash ]]; then
+  # valid-set ingest at C5 scale: timing line + per-kernel ncu metrics (profiles/hash/)
+  timeout 600 python scripts/profile_hash.py > "$OUT/hash_time.json" 2> "$OUT/hash_time.err"
+  timeout 900 ncu --metrics lts__t_sector_hit_rate.pct,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum \
+      --clock-control none --csv -k regex:'hash|valid|scatter|dense|lookup' \
+      python scripts/profile_hash.py --once > "$OUT/hash_ncu.csv" 2> "$OUT/hash_ncu.err"
+  echo "exit=$?" >> "$OUT/hash_ncu.err"
+fi
+
+if [[ $WHAT == ref ]]; then
+  timeout 1200 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 \
+      > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
+  echo "exit=$?" >> "$OUT/bench_ref.err"
 fi
 
 if [[ $WHAT == ab ]]; then

@@ -259,6 +259,43 @@ def test_staged_and_v1_paths_match_oracle(tk, monkeypatch, path, radix, q):
     assert it == rit and rel_l1(r, rr) <= PR_RTOL
 
 
+# Row-tiled PageRank (tk_rows.cu): shapes whose trailing dims span 16 ranks,
+# one per in-row structure, plus odd column lengths (tiles straddling columns)
+# and the C2 shape; the staged kernel (TK_PR_ROWS=0) on the same shapes.
+@pytest.mark.parametrize("rows", ["rows", "rows_win", "staged"])
+@pytest.mark.parametrize("radix,q", [
+    ([8, 6, 6, 4, 4, 4, 2, 2], 0.1),      # C5's trailing dims (4,2,2)
+    ([6, 8, 8, 4, 4], 0.2),               # (4,4)
+    ([3] + [2] * 10, 0.3),                # (2,2,2,2)
+    ([12, 12, 16, 16], 0.0),              # (16)
+    ([8, 8, 8, 8, 2], 0.1),               # (8,2)
+    ([16, 12, 2, 8], 0.1),                # (2,8)
+    ([8, 12, 10, 2, 4, 2], 0.2),          # (2,4,2), column of 5*... rows
+    ([5, 16, 8, 2, 2, 4], 0.2),           # (2,2,4)
+    ([7, 8, 4, 3, 4, 2, 2], 0.25),        # odd radices: super-columns, straddling tiles
+    ([16, 12, 8, 8, 8, 4, 2, 2], 0.3),    # C2 shape
+])
+def test_row_tiled_pagerank_matches_oracle(tk, monkeypatch, rows, radix, q):
+    monkeypatch.setenv("TK_PR_ROWS", "0" if rows == "staged" else "1")
+    if rows == "rows_win":  # the largest window the ring allows, however few columns
+        monkeypatch.setenv("TK_ROW_MINCOLS", "1")
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, q, 29)
+    if q == 0.0:
+        ok[:] = 1
+    ref = O.analyze(radix, fit, ok, O.ADJACENT, nthreads=8, node_limit=1 << 32)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        s = land.analyze(tk.ADJACENT, node_limit=1 << 32)
+        r = land.pagerank_vector()
+        info = land.kernel_info()
+    assert info["pagerank_kernel"] == rows.split("_")[0]
+    assert s.iterations == ref["iterations"]
+    assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
+    for k, c in ref["c_p_curve"]:
+        assert abs(s.c_p[k] - c) <= CP_ATOL
+
+
 @pytest.mark.parametrize("path", ["tiled", "v1"])
 @pytest.mark.parametrize("radix,q", [
     ([6, 6, 4, 4, 4, 4, 2, 2], 0.2),       # uniform / tile-aligned / per-thread digits
