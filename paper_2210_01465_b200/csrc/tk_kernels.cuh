@@ -238,13 +238,10 @@ struct RowPlan {
 };
 // TMA tensor maps of the rank-vector buffers viewed as [rows][16] f64 (SWIZZLE_128B)
 // and of the packed words as [rows][16] u32 (SWIZZLE_64B), 32-row boxes.
-// Loads use [rows][16] boxes; the consumer warps store half rows ([rows][8]
-// boxes, SWIZZLE_64B) of c' (cs) and of the closing r' pass (r0s).
 struct alignas(64) RowMaps {
     CUtensorMap c[2];
+    CUtensorMap r0;
     CUtensorMap pw;
-    CUtensorMap cs[2];
-    CUtensorMap r0s;
 };
 bool make_row_plan(const DevShape& s, int num_sms, RowPlan* plan);
 cudaError_t launch_pagerank_rows(const DevShape& s, const RowPlan& p, const PrArgs& a,

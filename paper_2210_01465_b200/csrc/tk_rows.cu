@@ -51,33 +51,38 @@ namespace cg = cooperative_groups;
 namespace tk {
 namespace {
 
-constexpr int kRowLen = 16;                      // ranks per row
-constexpr int kTileRows = 32;                    // rows per tile (one lane per row)
-constexpr int kRP = 4;                           // consumer warp pairs (tiles in flight)
+constexpr int kRowLen = 16;                      // ranks per row (one lane)
+constexpr int kTileRows = 32;                    // rows per tile (one consumer warp)
+#ifndef TK_ROW_WARPS
+#define TK_ROW_WARPS 8
+#endif
+constexpr int kRW = TK_ROW_WARPS;                // consumer warps = tiles in flight
 constexpr int kRingTiles = 16;                   // c ring: 16 tiles of 32 rows (64 KB)
 constexpr int kRingRows = kRingTiles * kTileRows;
 constexpr int kPwTiles = 8;                      // packed-word ring (2 KB per tile)
 #ifndef TK_ROW_FAR_SLOTS
-#define TK_ROW_FAR_SLOTS 8
+#define TK_ROW_FAR_SLOTS 3
 #endif
-constexpr int kFarSlots = TK_ROW_FAR_SLOTS;      // far ranges in flight per pair
-// consumer warps 0..2kRP-1 (pair w/2, half w&1: elements 8*half..+8 of every
-// row of the pair's tile) and producer warps 2kRP..3kRP-1 (one per pair)
-constexpr int kRowThreads = 3 * kRP * 32;
-static_assert(kRingTiles % kRP == 0 && kPwTiles % kRP == 0, "ring slots per producer");
+constexpr int kFarSlots = TK_ROW_FAR_SLOTS;      // far ranges in flight per consumer warp
+// consumer warps 0..kRW-1 (warp w: tiles i = w mod kRW, lane t = row t of the
+// tile, all 16 ranks of the row) and kRW/2 producer warps whose lanes 0 and 16
+// serve consumer warps 2p and 2p+1
+constexpr int kProdWarps = kRW / 2;
+constexpr int kRowThreads = (kRW + kProdWarps) * 32;
+static_assert(kRingTiles % kRW == 0 && kPwTiles % kRW == 0, "ring slots per producer");
 constexpr int kTileBytes = kTileRows * kRowLen * 8;  // 4 KB
-constexpr int kOutBytes = kTileBytes / 2;            // a half tile (32 x 64 B)
 constexpr int kPwTileBytes = kTileRows * kRowLen * 4;
 
 // dynamic shared memory map (1024-byte aligned regions: SWIZZLE_128B)
 constexpr int kOffRing = 0;
 constexpr int kOffFar = kOffRing + kRingTiles * kTileBytes;
-constexpr int kOffOut = kOffFar + kRP * kFarSlots * kTileBytes;
-constexpr int kOffPw = kOffOut + 2 * kRP * kOutBytes;
+constexpr int kOffOut = kOffFar + kRW * kFarSlots * kTileBytes;
+constexpr int kOffPw = kOffOut + kRW * kTileBytes;
 constexpr int kOffDesc = kOffPw + kPwTiles * kPwTileBytes;
 constexpr int kOffBar = kOffDesc + kPwTiles * 16;
-constexpr int kNumBars = 2 * kRingTiles + 2 * kPwTiles + 2 * kRP * kFarSlots;
+constexpr int kNumBars = 2 * kRingTiles + 2 * kPwTiles + 2 * kRW * kFarSlots;
 constexpr int kRowSmem = kOffBar + kNumBars * 8 + 1024;  // + alignment slack
+static_assert(kRowSmem <= 232448 - 512, "shared memory");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -111,6 +116,7 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
 // warp on its SM sub-partition
 __device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
     uint32_t done = 0;
+    const uint32_t ns = 64;
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -119,7 +125,7 @@ __device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
             : "=r"(done)
             : "r"(saddr(b)), "r"(parity), "r"(0x100000u)
             : "memory");
-        if (!done) __nanosleep(64);
+        if (!done) __nanosleep(ns);
     }
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -214,7 +220,7 @@ struct PrScalars {
 struct SweepState {
     uint32_t ring_base;  // global ring index of the sweep's entry 0
     uint32_t tile_base;  // block tiles of earlier sweeps (packed-word ring)
-    uint32_t far_ctr;    // far-slot counter of the pair (consumers + producer)
+    uint32_t far_ctr;    // far-slot counter of a consumer warp and its producer lane
 };
 
 struct RowCtx {
@@ -222,7 +228,7 @@ struct RowCtx {
     uint64_t* c_empty;
     uint64_t* pw_full;
     uint64_t* pw_empty;
-    uint64_t* far_full;   // [kRP][kFarSlots]
+    uint64_t* far_full;   // [kRW][kFarSlots]
     uint64_t* far_empty;
     uint8_t* ring;
     uint8_t* far;
@@ -255,9 +261,9 @@ __device__ __forceinline__ void far_dirs(const RowPlan& p, uint32_t r, uint32_t&
         if (p.far_span[d] || !(a == m - 1 && b == m - 1)) hi |= 1u << d;
     }
 }
-// far_dirs of a warp's tiles, recomputed only when the tile moves to another
-// column (when columns are whole tiles, every tile of a column has the same
-// far digits)
+// far_dirs of a producer's tiles, recomputed only when the tile moves to
+// another column (when columns are whole tiles, every tile of a column has
+// the same far digits)
 struct FarCache {
     uint32_t col = ~0u, lo = 0, hi = 0;
     __device__ __forceinline__ void get(const RowPlan& p, uint32_t i, uint32_t r, uint32_t& flo,
@@ -281,113 +287,108 @@ __device__ __forceinline__ void cadd(double& acc, double v, uint32_t m, uint32_t
     const uint32_t hi = (m & bit) ? 0x3FF00000u : 0u;
     acc = __fma_rn(v, __hiloint2double(static_cast<int>(hi), 0), acc);
 }
-// predicated 16-byte shared load (lanes with p == 0 issue no wavefront)
-__device__ __forceinline__ void lds2p(uint32_t a, double& x, double& y, uint32_t p) {
+// the 16 values of a 128-byte row: chunk q at base + off[q], one predicate
+// for all eight loads (lanes with p == 0 issue no wavefront)
+__device__ __forceinline__ void ld_row16(uint32_t base, const uint32_t (&off)[8], double (&v)[16],
+                                         uint32_t p) {
     asm volatile(
         "{\n\t.reg .pred q;\n\t"
-        "setp.ne.b32 q, %3, 0;\n\t"
-        "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
-        : "+d"(x), "+d"(y)
-        : "r"(a), "r"(p)
+        "setp.ne.b32 q, %24, 0;\n\t"
+        "@q ld.shared.v2.f64 {%0, %1}, [%16];\n\t"
+        "@q ld.shared.v2.f64 {%2, %3}, [%17];\n\t"
+        "@q ld.shared.v2.f64 {%4, %5}, [%18];\n\t"
+        "@q ld.shared.v2.f64 {%6, %7}, [%19];\n\t"
+        "@q ld.shared.v2.f64 {%8, %9}, [%20];\n\t"
+        "@q ld.shared.v2.f64 {%10, %11}, [%21];\n\t"
+        "@q ld.shared.v2.f64 {%12, %13}, [%22];\n\t"
+        "@q ld.shared.v2.f64 {%14, %15}, [%23];\n\t}"
+        : "+d"(v[0]), "+d"(v[1]), "+d"(v[2]), "+d"(v[3]), "+d"(v[4]), "+d"(v[5]), "+d"(v[6]),
+          "+d"(v[7]), "+d"(v[8]), "+d"(v[9]), "+d"(v[10]), "+d"(v[11]), "+d"(v[12]), "+d"(v[13]),
+          "+d"(v[14]), "+d"(v[15])
+        : "r"(base + off[0]), "r"(base + off[1]), "r"(base + off[2]), "r"(base + off[3]),
+          "r"(base + off[4]), "r"(base + off[5]), "r"(base + off[6]), "r"(base + off[7]), "r"(p)
         : "memory");
 }
 
-// Per-lane offsets of the 16-byte chunks of a 128-byte row whose SWIZZLE_128B
-// phase is the lane's own (t & 7): far ranges, the own row and every window
-// row at a multiple of 8 rows.  lo[q] = t * 128 + ((q ^ (t & 7)) << 4).
-struct LaneOff {
-    uint32_t lo[8];
-};
-
-// Consumer warp (pair, half H) of tile i: lane t owns elements [8H, 8H + 8)
-// of row r = tile_row + t; the pair's other warp owns the other half.  The
-// producer of the pair left the tile's first row and far directions in the
-// packed-word slot's descriptor.
-template <class RS, bool FINAL, int H>
+// One consumer warp handles tile i: lane t owns row r = r0 + t (16 ranks).
+// The producer lane of this warp left the tile's first row and far
+// directions in the packed-word slot's descriptor.
+template <class RS, bool FINAL>
 __device__ __forceinline__ void row_tile(const RowPlan& p, const RowMaps& maps, const RowCtx& cx,
-                                         const PrScalars& a, uint32_t i, uint32_t L, uint32_t e_i,
-                                         uint32_t pw_idx, uint32_t& far_ctr, int pr, int t,
-                                         const LaneOff& lo, double dn, int out_map, double& lres,
-                                         double& ldang, double& lsum, const double* s_rcp,
-                                         uint64_t pol_out) {
-    constexpr int E = 8;       // elements per lane
-    constexpr int J0 = 8 * H;  // first element of this half
+                                         const PrScalars& a, uint32_t i, uint32_t e_i,
+                                         uint32_t pw_idx, uint32_t& far_ctr, int w, int t,
+                                         const uint32_t (&lo)[8], double dn, int out_map,
+                                         double& lres, double& ldang, double& lsum,
+                                         const double* s_rcp, uint64_t pol_out) {
     const int D = p.dims;
     const int A = p.ahead;
-    // descriptor + packed words of this lane's 8 ranks (SWIZZLE_64B 64-byte rows)
-    uint32_t m[E];
-    uint32_t r0, flo, fhi;
+    uint32_t m[16];
+    uint32_t r0, flo, fhi, any;
     {
         const uint32_t ps = pw_idx % kPwTiles;
         bar_wait(cx.pw_full + ps, (pw_idx / kPwTiles) & 1u);
-        const uint4 dsc = cx.desc[ps];
-        r0 = dsc.x;
-        flo = dsc.y;
-        fhi = dsc.z;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r0), "=r"(flo), "=r"(fhi), "=r"(any)
+                     : "r"(saddr(cx.desc + ps))
+                     : "memory");
         const uint32_t base = saddr(cx.pwr + ps * kPwTileBytes) + t * 64;
         const uint32_t key = (t >> 1) & 3;
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-            lds4u(base + (((2 * H + q) ^ key) << 4), m[4 * q], m[4 * q + 1], m[4 * q + 2],
-                  m[4 * q + 3]);
+        for (int q = 0; q < 4; ++q)
+            lds4u(base + ((q ^ key) << 4), m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
         __syncwarp();
         if (t == 0) bar_arrive(cx.pw_empty + ps);
     }
-    uint32_t any = 0;
+    any = 0;
 #pragma unroll
-    for (int j = 0; j < E; ++j) any |= m[j];
-    // ring tiles i-A .. i+A (global ring index e_i + k); the sweep's first A
-    // tiles have no tiles before them (their lower window neighbours do not exist)
-    for (int k = (static_cast<int>(i) >= A ? -A : -static_cast<int>(i)); k <= A; ++k) {
+    for (int j = 0; j < 16; ++j) any |= m[j];
+    // ring tiles i-A .. i+A; the sweep's first A tiles have no tiles before
+    // them (their lower window neighbours do not exist)
+    const int k0 = static_cast<int>(i) >= A ? -A : -static_cast<int>(i);
+    for (int k = k0; k <= A; ++k) {
         const uint32_t e = e_i + k;
         bar_wait(cx.c_full + (e % kRingTiles), (e / kRingTiles) & 1u);
     }
     const uint32_t ring = saddr(cx.ring);
     const uint32_t rrow0 = (e_i % kRingTiles) * kTileRows;  // ring row of lane 0's row
-    const uint32_t far_p = saddr(cx.far + pr * kFarSlots * kTileBytes);
-    uint64_t* ffull = cx.far_full + pr * kFarSlots;
-    uint64_t* fempty = cx.far_empty + pr * kFarSlots;
+    const uint32_t far_w = saddr(cx.far + w * kFarSlots * kTileBytes);
+    uint64_t* ffull = cx.far_full + w * kFarSlots;
+    uint64_t* fempty = cx.far_empty + w * kFarSlots;
     uint32_t fs = far_ctr % kFarSlots, fph = (far_ctr / kFarSlots) & 1u;
 
-    double acc[E];
+    double acc[16];
 #pragma unroll
-    for (int j = 0; j < E; ++j) acc[j] = 0.0;
-    double v[E];
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    double v[16];
 #pragma unroll
-    for (int j = 0; j < E; ++j) v[j] = 0.0;
+    for (int j = 0; j < 16; ++j) v[j] = 0.0;
     auto addv = [&](uint32_t bit) {
 #pragma unroll
-        for (int j = 0; j < E; ++j) cadd(acc[j], v[j], m[j], bit);
+        for (int j = 0; j < 16; ++j) cadd(acc[j], v[j], m[j], bit);
     };
-    // this half's 8 values of a row at base + lo[q] (uniform base, lane phase t & 7)
-    auto ld_lane = [&](uint32_t base, uint32_t pred) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) lds2p(base + lo.lo[4 * H + q], v[2 * q], v[2 * q + 1], pred);
-    };
-    // a far range: wait for its slot, read this lane's half row, release (both halves arrive)
+    // a far range: wait for its slot, read this lane's row, release it
     auto far_take = [&](uint32_t bit) {
         bar_wait(ffull + fs, fph);
-        ld_lane(far_p + fs * kTileBytes, any & bit);
+        ld_row16(far_w + fs * kTileBytes, lo, v, any & bit);
         __syncwarp();
         if (t == 0) bar_arrive(fempty + fs);
         if (++fs == kFarSlots) {
             fs = 0;
             fph ^= 1u;
         }
-        ++far_ctr;
     };
     // a window direction: ring row of lane t = rrow0 + t + drow
     auto win_take = [&](int drow, uint32_t bit) {
         const uint32_t pred = any & bit;
+        const uint32_t rr = (rrow0 + t + kRingRows + drow) % kRingRows;
         if ((drow & 7) == 0) {  // same swizzle phase as the lane's own row
-            const uint32_t rr = (rrow0 + t + kRingRows + drow) % kRingRows;
-            ld_lane(ring + rr * 128 - t * 128, pred);
+            ld_row16(ring + rr * 128 - t * 128, lo, v, pred);
         } else {
-            const uint32_t rr = (rrow0 + t + kRingRows + drow) % kRingRows;
-            const uint32_t rb = ring + rr * 128, key = rr & 7;
+            const uint32_t key = rr & 7;
+            uint32_t o2[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                lds2p(rb + (((4 * H + q) ^ key) << 4), v[2 * q], v[2 * q + 1], pred);
+            for (int q = 0; q < 8; ++q) o2[q] = (q ^ key) << 4;
+            ld_row16(ring + rr * 128, o2, v, pred);
         }
     };
     // ---- lower neighbours (ascending rank): far dims, then window dims
@@ -403,48 +404,30 @@ __device__ __forceinline__ void row_tile(const RowPlan& p, const RowMaps& maps, 
         win_take(-p.win_rows[wk], bit);
         addv(bit);
     }
-    // ---- in-row neighbours: lower (ascending dim), then upper (descending dim);
-    // this half's own values plus the other half's where a row dim crosses halves
+    // ---- in-row neighbours from the own row: lower (ascending dim), then
+    // upper (descending dim)
     double own[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) own[j] = 0.0;
+    ld_row16(ring + rrow0 * 128, lo, own, 1u);
     {
-        const uint32_t base = ring + rrow0 * 128;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            bool need = q / 4 == H;  // chunk q holds elements 2q, 2q+1
-#pragma unroll
-            for (int jj = 0; jj < E; ++jj) {
-                const int j = J0 + jj;
-#pragma unroll
-                for (int k = 0; k < RS::nd; ++k) {
-                    const int dg = RS::digit(j, k), st = RS::stride(k);
-                    if (dg > 0 && (j - st) / 2 == q) need = true;
-                    if (dg < RS::radix(k) - 1 && (j + st) / 2 == q) need = true;
-                }
-            }
-            if (need) lds2p(base + lo.lo[q], own[2 * q], own[2 * q + 1], 1u);
-            else own[2 * q] = own[2 * q + 1] = 0.0;
-        }
         const int d0 = D - RS::nd;  // first row dim
 #pragma unroll
         for (int k = 0; k < RS::nd; ++k) {
             const uint32_t bit = 1u << (d0 + k);
 #pragma unroll
-            for (int jj = 0; jj < E; ++jj) {
-                const int j = J0 + jj;
+            for (int j = 0; j < 16; ++j)
                 if (RS::digit(j, k) > 0)
-                    cadd(acc[jj], own[RS::digit(j, k) > 0 ? j - RS::stride(k) : j], m[jj], bit);
-            }
+                    cadd(acc[j], own[RS::digit(j, k) > 0 ? j - RS::stride(k) : j], m[j], bit);
         }
 #pragma unroll
         for (int k = RS::nd - 1; k >= 0; --k) {
             const uint32_t bit = 1u << (2 * D - 1 - (d0 + k));
 #pragma unroll
-            for (int jj = 0; jj < E; ++jj) {
-                const int j = J0 + jj;
+            for (int j = 0; j < 16; ++j)
                 if (RS::digit(j, k) < RS::radix(k) - 1)
-                    cadd(acc[jj], own[RS::digit(j, k) < RS::radix(k) - 1 ? j + RS::stride(k) : j],
-                         m[jj], bit);
-            }
+                    cadd(acc[j], own[RS::digit(j, k) < RS::radix(k) - 1 ? j + RS::stride(k) : j],
+                         m[j], bit);
         }
     }
     // ---- upper neighbours (ascending rank): window dims (descending), far dims (descending)
@@ -462,50 +445,35 @@ __device__ __forceinline__ void row_tile(const RowPlan& p, const RowMaps& maps, 
         far_take(bit);
         addv(bit);
     }
-    // release the ring tiles this tile read.  Ring tile j (sweep-local) has
-    // 2A+1 users i-A..i+A (two warps each); the last real user also arrives
-    // for the ones that do not exist (before the sweep's first or after its
-    // last tile).
+    far_ctr += __popc(flo) + __popc(fhi);
+    // release the ring tiles this tile read (their missing users before the
+    // sweep's first / after its last tile were arrived for by the producer)
     __syncwarp();
-    if (t == 0) {
-        for (int k = -A; k <= A; ++k) {
-            const int j = static_cast<int>(i) + k;
-            if (j < 0) continue;
-            const int last = min(j + A, static_cast<int>(L) - 1);
-            uint32_t cnt = 1;
-            if (static_cast<int>(i) == last) {
-                const int first = max(j - A, 0);
-                cnt = static_cast<uint32_t>(2 * A + 1 - (last - first + 1) + 1);
-            }
-            bar_arrive(cx.c_empty + ((e_i + k) % kRingTiles), cnt);
-        }
-    }
-    // ---- epilogue: r' per rank, residual terms, c' (or r') out: this half's
-    // 32 x 64-byte block (SWIZZLE_64B) through one TMA store
-    const uint32_t ob = saddr(cx.out + (2 * pr + H) * kOutBytes) + t * 64;
-    const uint32_t okey = (t >> 1) & 3;
+    if (t == 0)
+        for (int k = k0; k <= A; ++k) bar_arrive(cx.c_empty + ((e_i + k) % kRingTiles));
+    // ---- epilogue: r' per rank, residual terms, c' (or r') out via one TMA store
+    const uint32_t ob = saddr(cx.out + w * kTileBytes);
     if (t == 0) tma_store_wait_read();  // the previous store from this buffer has read it
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 8; ++q) {
         double o[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int jj = 2 * q + h;
-            const uint32_t deg = m[jj] >> kPackedSlots;
-            const double x = __dadd_rn(a.teleport, __dmul_rn(a.damping, __dadd_rn(acc[jj], dn)));
+            const int j = 2 * q + h;
+            const uint32_t deg = m[j] >> kPackedSlots;
+            const double x = __dadd_rn(a.teleport, __dmul_rn(a.damping, __dadd_rn(acc[j], dn)));
             if (FINAL) {
                 o[h] = x;
             } else {
-                const double cold = own[J0 + jj];
                 double qv, dv;
                 if (deg) {
                     const double dd = static_cast<double>(deg);
                     qv = div_small_r(x, dd, s_rcp[deg]);
-                    dv = fabs(__fma_rn(cold, dd, -x));
+                    dv = fabs(__fma_rn(own[j], dd, -x));
                 } else {
                     qv = x;  // a sink's slot carries its rank (no pull reads it)
-                    dv = fabs(__dsub_rn(x, cold));
+                    dv = fabs(__dsub_rn(x, own[j]));
                     ldang = __dadd_rn(ldang, x);
                 }
                 lres = __dadd_rn(lres, dv);
@@ -513,14 +481,90 @@ __device__ __forceinline__ void row_tile(const RowPlan& p, const RowMaps& maps, 
                 o[h] = qv;
             }
         }
-        sts2(ob + ((q ^ okey) << 4), o[0], o[1]);
+        sts2(ob + lo[q], o[0], o[1]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (t == 0) {
-        const CUtensorMap* om = out_map == 2 ? &maps.r0s : &maps.cs[out_map];
-        tma_store_half(om, 8 * H, static_cast<int>(r0), cx.out + (2 * pr + H) * kOutBytes, pol_out);
+        const CUtensorMap* om = out_map == 2 ? &maps.r0 : &maps.c[out_map];
+        tma_store_rows(om, static_cast<int>(r0), cx.out + w * kTileBytes, pol_out);
     }
+}
+
+// Producer lane of consumer warp w: for each of its tiles i, ring entry i + A
+// (the tile A ahead enters the c window), the packed words + descriptor of
+// tile i, and its far ranges.  Ring / packed-word slots are multiples of kRW
+// apart, so a slot's loads always come from one producer lane, in order.
+// Ring entry j (sweep-local) has 2A+1 users (tiles j-A..j+A); the users that
+// do not exist (before tile 0, after tile L-1) are arrived for here.
+__device__ __forceinline__ void row_produce(const RowPlan& p, const RowMaps& maps,
+                                            const RowCtx& cx, uint32_t L, uint32_t LE,
+                                            uint32_t ring_base, uint32_t tile_base,
+                                            uint32_t& far_ctr, int w, int in_map) {
+    const uint64_t pol = policy_evict_normal();
+    const uint64_t pol_ef = policy_evict_first();
+    const CUtensorMap* cm = &maps.c[in_map];
+    const int A = p.ahead;
+    uint8_t* far_w = cx.far + w * kFarSlots * kTileBytes;
+    uint64_t* ffull = cx.far_full + w * kFarSlots;
+    uint64_t* fempty = cx.far_empty + w * kFarSlots;
+    uint32_t fc = far_ctr;
+    uint32_t fs = fc % kFarSlots, fph = (fc / kFarSlots) & 1u;
+    FarCache fcache;
+    auto ring_entry = [&](uint32_t j) {
+        const uint32_t e = ring_base + j;
+        const uint32_t slot = e % kRingTiles;
+        if (e >= kRingTiles) bar_wait_sleep(cx.c_empty + slot, ((e / kRingTiles) + 1) & 1u);
+        // users j-A..j+A outside [0, L)
+        const int lo_missing = static_cast<int>(j) < A ? A - static_cast<int>(j) : 0;
+        const int hi_missing = static_cast<int>(j + A) >= static_cast<int>(L)
+                                   ? static_cast<int>(j + A) - static_cast<int>(L) + 1
+                                   : 0;
+        const int missing = min(lo_missing + hi_missing, 2 * A + 1);
+        if (missing) bar_arrive(cx.c_empty + slot, static_cast<uint32_t>(missing));
+        if (j < L) {
+            bar_expect(cx.c_full + slot, kTileBytes);
+            tma_load_rows(cx.ring + slot * kTileBytes, cm, static_cast<int>(tile_row(p, j)),
+                          cx.c_full + slot, pol);
+        } else {
+            bar_arrive(cx.c_full + slot);  // overhang entry: nothing to load
+        }
+    };
+    auto issue = [&](int row, int d) {
+        if (fc >= kFarSlots) bar_wait_sleep(fempty + fs, fph ^ 1u);
+        bar_expect(ffull + fs, kTileBytes);
+        tma_load_rows(far_w + fs * kTileBytes, cm, row, ffull + fs,
+                      ((p.far_ef >> d) & 1u) ? pol_ef : pol);
+        ++fc;
+        if (++fs == kFarSlots) {
+            fs = 0;
+            fph ^= 1u;
+        }
+    };
+    if (w < A && static_cast<uint32_t>(w) < LE) ring_entry(w);  // the sweep's first A entries
+    for (uint32_t i = w; i < L; i += kRW) {
+        ring_entry(i + A);
+        const uint32_t r = tile_row(p, i);
+        const uint32_t pi = tile_base + i;
+        const uint32_t ps = pi % kPwTiles;
+        uint32_t lo, hi;
+        fcache.get(p, i, r, lo, hi);
+        if (pi >= kPwTiles) bar_wait_sleep(cx.pw_empty + ps, ((pi / kPwTiles) + 1) & 1u);
+        cx.desc[ps] = make_uint4(r, lo, hi, 0);  // released by the arrive below
+        bar_expect(cx.pw_full + ps, kPwTileBytes);
+        tma_load_rows(cx.pwr + ps * kPwTileBytes, &maps.pw, static_cast<int>(r), cx.pw_full + ps,
+                      pol_ef);
+        for (uint32_t rem = lo; rem; rem &= rem - 1) {
+            const int d = __ffs(rem) - 1;
+            issue(static_cast<int>(r) - static_cast<int>(p.far_rows[d]), d);
+        }
+        for (uint32_t rem = hi; rem;) {
+            const int d = 31 - __clz(rem);
+            rem ^= 1u << d;
+            issue(static_cast<int>(r + p.far_rows[d]), d);
+        }
+    }
+    far_ctr = fc;
 }
 
 template <class RS, bool FINAL>
@@ -530,101 +574,31 @@ __device__ __forceinline__ void row_sweep(const RowPlan& p, const RowMaps& maps,
                                           double& lres_out, double& ldang_out, double& lsum_out,
                                           const double* s_rcp) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t ring_base = ss.ring_base, tile_base = ss.tile_base;
-    uint32_t far_ctr = ss.far_ctr;
-    double lres = 0.0, ldang = 0.0, lsum = 0.0;  // registers; added to the outputs at the end
-    {
-        if (warp >= 2 * kRP) {  // --------------------------------- producer of pair pr
-            // Producer pr serves the tiles i = pr (mod kRP) of its consumer pair:
-            // ring entry i + A (the tile A ahead enters the c window), the packed
-            // words of tile i and its far ranges.  Ring entry / packed-word slots
-            // are multiples of kRP apart, so a slot's loads always come from one
-            // producer, in order (no phase can be skipped).
-            const int pr = warp - 2 * kRP;
-            if (lane == 0) {
-                const uint64_t pol = policy_evict_normal();
-                const uint64_t pol_ef = policy_evict_first();
-                const CUtensorMap* cm = &maps.c[in_map];
-                const int A = p.ahead;
-                uint8_t* far_p = cx.far + pr * kFarSlots * kTileBytes;
-                uint64_t* ffull = cx.far_full + pr * kFarSlots;
-                uint64_t* fempty = cx.far_empty + pr * kFarSlots;
-                uint32_t fc = far_ctr;
-                FarCache fcache;
-                auto ring_entry = [&](uint32_t j) {
-                    const uint32_t e = ring_base + j;
-                    const uint32_t slot = e % kRingTiles;
-                    if (e >= kRingTiles) bar_wait_sleep(cx.c_empty + slot, ((e / kRingTiles) + 1) & 1u);
-                    if (j < L) {
-                        bar_expect(cx.c_full + slot, kTileBytes);
-                        tma_load_rows(cx.ring + slot * kTileBytes, cm,
-                                      static_cast<int>(tile_row(p, j)), cx.c_full + slot, pol);
-                    } else {
-                        bar_arrive(cx.c_full + slot);  // overhang entry: nothing to load
-                    }
-                };
-                auto issue = [&](int row, int d) {
-                    const uint32_t s = fc % kFarSlots;
-                    if (fc >= kFarSlots) bar_wait_sleep(fempty + s, ((fc / kFarSlots) + 1) & 1u);
-                    bar_expect(ffull + s, kTileBytes);
-                    tma_load_rows(far_p + s * kTileBytes, cm, row, ffull + s,
-                                  ((p.far_ef >> d) & 1u) ? pol_ef : pol);
-                    ++fc;
-                };
-                if (pr < A && static_cast<uint32_t>(pr) < LE) ring_entry(pr);  // the sweep's first A entries
-                for (uint32_t i = pr; i < L; i += kRP) {
-                    ring_entry(i + A);
-                    const uint32_t r = tile_row(p, i);
-                    const uint32_t pi = tile_base + i;
-                    const uint32_t ps = pi % kPwTiles;
-                    uint32_t lo, hi;
-                    fcache.get(p, i, r, lo, hi);
-                    if (pi >= kPwTiles) bar_wait_sleep(cx.pw_empty + ps, ((pi / kPwTiles) + 1) & 1u);
-                    cx.desc[ps] = make_uint4(r, lo, hi, 0);  // released by the arrive below
-                    bar_expect(cx.pw_full + ps, kPwTileBytes);
-                    tma_load_rows(cx.pwr + ps * kPwTileBytes, &maps.pw, static_cast<int>(r),
-                                  cx.pw_full + ps, pol_ef);
-                    for (uint32_t rem = lo; rem; rem &= rem - 1) {
-                        const int d = __ffs(rem) - 1;
-                        issue(static_cast<int>(r) - static_cast<int>(p.far_rows[d]), d);
-                    }
-                    for (uint32_t rem = hi; rem;) {
-                        const int d = 31 - __clz(rem);
-                        rem ^= 1u << d;
-                        issue(static_cast<int>(r + p.far_rows[d]), d);
-                    }
-                }
-                far_ctr = fc;
-            }
-        } else {  // ---------------------------------------- consumer warp (pair, half)
-            const int pr = warp >> 1, half = warp & 1;
-            const uint64_t pol_out = policy_evict_first();
-            LaneOff lo;
+    double lres = 0.0, ldang = 0.0, lsum = 0.0;
+    if (warp >= kRW) {  // producer warps: lanes 0 and 16 serve consumer warps 2p, 2p+1
+        if ((lane & 15) == 0)
+            row_produce(p, maps, cx, L, LE, ss.ring_base, ss.tile_base, ss.far_ctr,
+                        2 * (warp - kRW) + (lane >> 4), in_map);
+    } else {
+        const uint64_t pol_out = policy_evict_first();
+        uint32_t lo[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) lo.lo[q] = lane * 128 + ((q ^ (lane & 7)) << 4);
-            for (uint32_t i = pr; i < L; i += kRP) {
-#define TK_ROW_TILE(FIN, HH)                                                                      \
-    row_tile<RS, FIN, HH>(p, maps, cx, sc, i, L, ring_base + i, tile_base + i, far_ctr, pr, lane, \
-                          lo, dn, out_map, lres, ldang, lsum, s_rcp, pol_out)
-                if (half) TK_ROW_TILE(FINAL, 1);
-                else TK_ROW_TILE(FINAL, 0);
-#undef TK_ROW_TILE
-            }
-            if (lane == 0) {
-                tma_store_wait_all();  // c' complete before the grid barrier
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-            }
-            __syncwarp();
+        for (int q = 0; q < 8; ++q) lo[q] = lane * 128 + ((q ^ (lane & 7)) << 4);
+        for (uint32_t i = warp; i < L; i += kRW)
+            row_tile<RS, FINAL>(p, maps, cx, sc, i, ss.ring_base + i, ss.tile_base + i, ss.far_ctr,
+                                warp, lane, lo, dn, out_map, lres, ldang, lsum, s_rcp, pol_out);
+        if (lane == 0) {
+            tma_store_wait_all();  // c' complete before the grid barrier
+            asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        __syncwarp();
     }
-    ss.ring_base = ring_base + LE;
-    ss.tile_base = tile_base + L;
-    ss.far_ctr = far_ctr;
+    ss.ring_base += LE;
+    ss.tile_base += L;
     lres_out = __dadd_rn(lres_out, lres);
     ldang_out = __dadd_rn(ldang_out, ldang);
     lsum_out = __dadd_rn(lsum_out, lsum);
 }
-
 
 __device__ __forceinline__ double reduce_parts_r(const double* part, int nblocks, int k,
                                                  double* s_red) {
@@ -645,7 +619,6 @@ __global__ void __launch_bounds__(kRowThreads, 1)
     __shared__ double s_red[kRowThreads / 32];
     __shared__ double s_rcp[kPackedSlots + 1];
     const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
     if (t <= kPackedSlots) s_rcp[t] = t ? __drcp_rn(static_cast<double>(t)) : 0.0;
     RowCtx cx;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -654,7 +627,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
     cx.pw_full = cx.c_empty + kRingTiles;
     cx.pw_empty = cx.pw_full + kPwTiles;
     cx.far_full = cx.pw_empty + kPwTiles;
-    cx.far_empty = cx.far_full + kRP * kFarSlots;
+    cx.far_empty = cx.far_full + kRW * kFarSlots;
     cx.ring = smem + kOffRing;
     cx.far = smem + kOffFar;
     cx.out = smem + kOffOut;
@@ -667,15 +640,15 @@ __global__ void __launch_bounds__(kRowThreads, 1)
     if (t == 0) {
         for (int k = 0; k < kRingTiles; ++k) {
             bar_init(cx.c_full + k, 1);
-            bar_init(cx.c_empty + k, 2 * (2 * p.ahead + 1));
+            bar_init(cx.c_empty + k, 2 * p.ahead + 1);
         }
         for (int k = 0; k < kPwTiles; ++k) {
             bar_init(cx.pw_full + k, 1);
-            bar_init(cx.pw_empty + k, 2);
+            bar_init(cx.pw_empty + k, 1);
         }
-        for (int k = 0; k < kRP * kFarSlots; ++k) {
+        for (int k = 0; k < kRW * kFarSlots; ++k) {
             bar_init(cx.far_full + k, 1);
-            bar_init(cx.far_empty + k, 2);
+            bar_init(cx.far_empty + k, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -831,9 +804,9 @@ bool make_row_plan(const DevShape& s, int num_sms, RowPlan* out) {
     if (dr < 1) return false;
     const uint64_t rows = s.n / kRowLen;
     // window: dims F..dr-1 (the largest suffix) with lookahead A = ceil(stride_rows(F) / 32)
-    // small enough for the ring (2A + kRP + 4 <= kRingTiles), at least 2 columns per
+    // small enough for the ring (2A + kRW + 2 <= kRingTiles), at least 2 columns per
     // CTA, and a column-group ("super-column", a whole number of 32-row tiles) length
-    int maxA = (kRingTiles - kRP - 4) / 2;
+    int maxA = (kRingTiles - kRW - 2) / 2;
     if (const char* e = std::getenv("TK_ROW_MAXA")) maxA = std::max(0, std::min(maxA, std::atoi(e)));
     uint64_t min_cols = static_cast<uint64_t>(2 * num_sms);  // keep every SM busy
     if (const char* e = std::getenv("TK_ROW_MINCOLS")) min_cols = std::strtoull(e, nullptr, 0);
@@ -895,8 +868,7 @@ cudaError_t launch_pagerank_rows(const DevShape& s, const RowPlan& p, const PrAr
     std::memset(&maps, 0, sizeof(maps));
     const uint64_t rows = p.rows;
     if (!encode_rows(&maps.c[0], a.c0, rows, true) || !encode_rows(&maps.c[1], a.c1, rows, true) ||
-        !encode_rows(&maps.pw, a.pw, rows, false) || !encode_rows(&maps.cs[0], a.c0, rows, true, 8) ||
-        !encode_rows(&maps.cs[1], a.c1, rows, true, 8) || !encode_rows(&maps.r0s, a.r0, rows, true, 8))
+        !encode_rows(&maps.pw, a.pw, rows, false) || !encode_rows(&maps.r0, a.r0, rows, true))
         return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
     if (e != cudaSuccess) return e;
