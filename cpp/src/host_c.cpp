@@ -1,9 +1,8 @@
 // host_c.cpp -- C-linkage access to the drop-in's host-side generators, so
 // non-C++ callers (bench.py's C4 batch) can build reference-identical
-// synthetic caches (generators.cpp restates /root/reference/proj/src/
-// generators.cpp:89-145 bit for bit).
+// synthetic caches (the reference's own generators.cpp:89-145, linked from
+// its sources -- cpp/Makefile).
 #include <cstdint>
-#include <cstring>
 #include <string>
 #include <vector>
 
@@ -24,8 +23,10 @@ extern "C" int tk_host_generate_synthetic(uint32_t dims, const uint32_t* radix, 
         }
         const SearchSpaceCache c = generate_synthetic_kernel_space(
             ParameterSpace(std::move(ps)), fail_fraction, synthetic_profile(profile), seed);
-        std::memcpy(fitness, c.mean_data(), c.size() * sizeof(double));
-        std::memcpy(ok, c.ok_data(), c.size());
+        for (std::uint64_t r = 0; r < c.size(); ++r) {
+            fitness[r] = c.mean(r);
+            ok[r] = c.ok(r) ? 1 : 0;
+        }
         return 0;
     } catch (const InvalidArgument&) {
         return 1;

@@ -5,9 +5,10 @@
 // cache, maps status codes onto the reference's exceptions and shapes the
 // results into the reference's structs.
 //
-// It compiles against either header set: this repo's include/tunekit/ or the
-// reference's own proj/include/tunekit/ (tests/test_cpp_dropin.py links the
-// latter against the reference's src/*.cpp as a conformance check).
+// It is compiled against the reference's own proj/include/tunekit/ headers and
+// linked with the reference's own host classes (value/space/cache/generators/
+// cache_io .cpp, built where they lie -- cpp/Makefile): this repo ships only
+// the landscape implementation, not copies of the reference's sources.
 #include "tunekit/landscape.hpp"
 
 #include <algorithm>
@@ -70,9 +71,6 @@ Land upload(const SearchSpaceCache& cache) {
     tk_land* raw = nullptr;
     check(tk_land_create(device_index(), static_cast<std::uint32_t>(radix.size()), radix.data(), &raw));
     Land land(raw);
-#ifdef TUNEKIT_B200_DENSE_CACHE
-    check(tk_land_load_dense(land.get(), cache.mean_data(), cache.ok_data(), TK_MEM_HOST));
-#else
     const std::uint64_t n = cache.size();
     std::vector<double> fit(n);
     std::vector<std::uint8_t> ok(n);
@@ -81,18 +79,13 @@ Land upload(const SearchSpaceCache& cache) {
         ok[r] = cache.ok(r) ? 1 : 0;
     }
     check(tk_land_load_dense(land.get(), fit.data(), ok.data(), TK_MEM_HOST));
-#endif
     return land;
 }
 
 std::vector<double> fitness_of(const SearchSpaceCache& cache) {
-#ifdef TUNEKIT_B200_DENSE_CACHE
-    return std::vector<double>(cache.mean_data(), cache.mean_data() + cache.size());
-#else
     std::vector<double> f(cache.size());
     for (std::uint64_t r = 0; r < cache.size(); ++r) f[r] = cache.mean(r);
     return f;
-#endif
 }
 
 }  // namespace

@@ -1,5 +1,6 @@
 // test_dropin -- drives the C++ drop-in (tunekit/landscape.hpp over the C-ABI)
-// on a GPU the way a reference user would, and dumps every result for
+// on a GPU the way a reference user would -- built against the reference's own
+// headers and host classes (cpp/Makefile) -- and dumps every result for
 // tests/test_cpp_dropin.py to compare with the CPU oracle:
 //   test_dropin <outdir> <q> <profile> <seed> <m0> <m1> ...
 #include <cstdio>
@@ -73,6 +74,7 @@ int main(int argc, char** argv) {
         const MinimaFractionReport mf = minima_fraction_report(cache, kind);
         std::ofstream fr(dir + "/fraction_" + k + ".txt");
         fr << std::hexfloat << mf.median << ' ' << mf.mean << ' ' << mf.fractions.size() << '\n';
+        dump(dir + "/fraction_" + k + ".bin", mf.fractions);
         EXPECT(rep.minima.size() == g.minima.size());
         EXPECT(mf.fractions.size() == g.minima.size());
         if (kind == NeighbourhoodKind::Adjacent) {

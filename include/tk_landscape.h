@@ -2,8 +2,8 @@
  * tk_landscape.h -- the C-ABI drop-in boundary for the FFG / PageRank / C_p path.
  *
  * Plain C: pointers, sizes, status codes.  No exceptions, no torch or C++ types
- * cross this boundary.  The C++ drop-in (include/tunekit/landscape.hpp, built on
- * top of this ABI) rethrows the status codes as the reference's exception types.
+ * cross this boundary.  The C++ drop-in (cpp/src/landscape.cpp, the reference's
+ * include/tunekit/landscape.hpp implemented on top of this ABI) rethrows the status codes as the reference's exception types.
  *
  * Every entry point names the reference interface it replaces.  Paths are
  * relative to /root/reference/proj (read-only reference; the declarations there
