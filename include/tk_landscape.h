@@ -157,6 +157,19 @@ int tk_analyze(tk_land* land, int kind, double damping, double tol, int64_t max_
                uint64_t node_limit, int p_max_percent, int emit_csr,
                tk_report_summary* out);
 
+/* ------------------------------- random-walk validator -- */
+/* hillclimb.cpp:48-87 climb_random_first, batched on the device: `walkers`
+ * randomized first-improvement descents from uniform starts over the loaded
+ * table, in the neighbourhood of the last tk_ffg_build (the
+ * paper's s7.2 random-walk claim).  Walker w draws from its own splitmix64
+ * stream (seed, w); results are deterministic and bit-identical to the
+ * oracle's restatement.  arrivals: n_minima u64, the descents that ended at
+ * each FFG minimum (tk_ffg_copy_out order); fail_arrivals: those that ended on
+ * a failed sink; evaluations: fitness lookups made.  Any output may be NULL.
+ * At most 256 neighbour slots (build_slots).  TK_ESTATE before a build. */
+int tk_descents(tk_land* land, uint64_t walkers, uint64_t seed, int restart_scan,
+                uint64_t* arrivals, uint64_t* fail_arrivals, uint64_t* evaluations);
+
 /* ------------------------------------- key-range sharding -- */
 /* Multi-GPU analyze_landscape: one handle per GPU, every handle loads the full
  * fitness table, handle `rank` of `nranks` owns ranks [lo, hi) (lo = rank *
@@ -164,7 +177,10 @@ int tk_analyze(tk_land* land, int kind, double damping, double tol, int64_t max_
  * 2*dims <= 27 only.  After tk_land_set_shard, tk_ffg_build builds the
  * shard's rows only (n_edges / n_minima are the shard's counts, no CSR).
  * The host sums the per-shard partials across ranks between calls (see
- * paper_2210_01465_b200/sharded.py); that reduction is the iteration barrier. */
+ * paper_2210_01465_b200/sharded.py); that reduction is the iteration barrier.
+ * The whole-space calls (tk_optimum, tk_ffg_copy_out of offsets / targets /
+ * is_sink, tk_census, tk_pagerank, tk_centrality, tk_analyze) return
+ * TK_ESTATE on a sharded handle: its rows cover only [lo, hi). */
 int tk_land_set_shard(tk_land* land, int rank, int nranks, uint64_t* lo, uint64_t* hi);
 /* device pointers of this handle's two PageRank contribution replicas */
 int tk_land_replica_ptrs(tk_land* land, void** c0, void** c1);

@@ -69,6 +69,8 @@ def lib():
         L.or_gen_synthetic.argtypes = [C.c_uint32, _u32p, C.c_double, C.c_double,
                                        C.c_double, C.c_double, C.c_uint64, _f64p, _u8p,
                                        C.c_int]
+        L.or_descents.argtypes = [C.c_uint32, _u32p, _f64p, C.c_int, C.c_uint64, C.c_uint64,
+                                  C.c_int, _u32p, C.POINTER(C.c_uint64), C.c_int]
         _lib = L
     return _lib
 
@@ -211,6 +213,21 @@ def optimum(fit, ok):
     if st:
         raise OracleError(st, "optimum")
     return f.value, r.value
+
+
+def descents(radix, fit, kind, walkers, seed, restart_scan=True, nthreads=0):
+    """hillclimb.cpp:48-87 climb_random_first from `walkers` uniform starts
+    (oracle.c or_descents; same draws as the device validator).  Returns the
+    per-rank arrival counts (u32[N]) and the number of fitness evaluations."""
+    r = np.ascontiguousarray(radix, np.uint32)
+    fit = np.ascontiguousarray(fit, np.float64)
+    counts = np.zeros(fit.shape[0], np.uint32)
+    ev = C.c_uint64()
+    st = lib().or_descents(len(r), r, fit, kind, walkers, seed, int(restart_scan), counts,
+                           C.byref(ev), nthreads)
+    if st:
+        raise OracleError(st, "descents")
+    return counts, ev.value
 
 
 def census(radix, fit, ok, kind):

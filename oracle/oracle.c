@@ -630,3 +630,105 @@ int or_gen_synthetic(uint32_t dims, const uint32_t* radix, double fail_fraction,
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------ randomized descents --
+ * hillclimb.cpp:48-87 climb_random_first.  Slot universe (build_slots,
+ * hillclimb.cpp:26-38): per dimension ascending, Adjacent {-1, +1} when
+ * m > 1, Hamming the m-1 alternatives a (index a < x ? a : a + 1,
+ * resolve_slot :41-46).  The scan walks a random permutation of the slots
+ * cyclically; the first strictly better neighbour (fp64 <) is taken, and with
+ * restart_scan a fresh permutation starts after every move.  The descent
+ * stops after a full cycle without an improvement.
+ *
+ * Draws (shared with the device validator, tk_descent.cu): walker w owns the
+ * splitmix64 stream s_0 = sm(seed ^ sm(w)), next() = sm-step; uniform(k) =
+ * mulhi64(next(), k).  The start rank is the first draw; a permutation is
+ * Fisher-Yates from the identity, i = S-1 .. 1, swap(p[i], p[uniform(i+1)]). */
+static inline uint64_t or_sm_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static inline uint64_t or_sm_next(uint64_t* s) {
+    *s += 0x9E3779B97F4A7C15ULL;
+    return or_sm_mix(*s);
+}
+static inline uint64_t or_uniform(uint64_t* s, uint64_t k) {
+    return (uint64_t)(((unsigned __int128)or_sm_next(s) * k) >> 64);
+}
+
+int or_descents(uint32_t dims, const uint32_t* radix, const double* fit, int kind,
+                uint64_t walkers, uint64_t seed, int restart_scan, uint32_t* counts,
+                uint64_t* evaluations, int nthreads) {
+    uint64_t strides[64];
+    if (dims > 64) return OR_EINVAL;
+    const uint64_t n = or_space_strides(dims, radix, strides);
+    uint8_t sdim[256];
+    int16_t salt[256];
+    int S = 0;
+    for (uint32_t i = 0; i < dims; ++i) {
+        const int m = (int)radix[i];
+        if (kind == OR_HAMMING) {
+            for (int a = 0; a + 1 < m; ++a) {
+                if (S == 256) return OR_EINVAL;
+                sdim[S] = (uint8_t)i, salt[S++] = (int16_t)a;
+            }
+        } else if (m > 1) {
+            if (S + 2 > 256) return OR_EINVAL;
+            sdim[S] = (uint8_t)i, salt[S++] = -1;
+            sdim[S] = (uint8_t)i, salt[S++] = +1;
+        }
+    }
+    memset(counts, 0, n * sizeof(uint32_t));
+    uint64_t evals = 0;
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : evals)
+    for (int64_t w = 0; w < (int64_t)walkers; ++w) {
+        uint64_t st = or_sm_mix(seed ^ or_sm_mix((uint64_t)w));
+        uint64_t rank = or_uniform(&st, n);
+        double f = fit[rank];
+        if (S) {
+            int x[64];
+            uint64_t rem = rank;
+            for (uint32_t i = 0; i < dims; ++i) x[i] = (int)(rem / strides[i]), rem %= strides[i];
+            uint8_t order[256];
+            for (int i = 0; i < S; ++i) order[i] = (uint8_t)i;
+            for (int i = S - 1; i > 0; --i) {
+                const int j = (int)or_uniform(&st, (uint64_t)i + 1);
+                const uint8_t t = order[i]; order[i] = order[j]; order[j] = t;
+            }
+            int pos = 0, since = 0;
+            while (since < S) {
+                const int sl = order[pos];
+                pos = pos + 1 == S ? 0 : pos + 1;
+                const int d = sdim[sl], m = (int)radix[d], cur = x[d];
+                const int j = kind == OR_HAMMING ? (salt[sl] < cur ? salt[sl] : salt[sl] + 1)
+                                                 : cur + salt[sl];
+                if (j < 0 || j >= m) {
+                    ++since;
+                    continue;
+                }
+                const uint64_t nb = rank + (uint64_t)((int64_t)(j - cur) * (int64_t)strides[d]);
+                const double fn = fit[nb];
+                ++evals;
+                if (fn < f) {
+                    x[d] = j, rank = nb, f = fn, since = 0;
+                    if (restart_scan) {
+                        for (int i = 0; i < S; ++i) order[i] = (uint8_t)i;
+                        for (int i = S - 1; i > 0; --i) {
+                            const int r = (int)or_uniform(&st, (uint64_t)i + 1);
+                            const uint8_t t = order[i]; order[i] = order[r]; order[r] = t;
+                        }
+                        pos = 0;
+                    }
+                } else {
+                    ++since;
+                }
+            }
+        }
+#pragma omp atomic
+        counts[rank] += 1;
+    }
+    if (evaluations) *evaluations = evals;
+    return OR_OK;
+}

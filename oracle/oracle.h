@@ -81,6 +81,16 @@ int or_gen_synthetic(uint32_t dims, const uint32_t* radix, double fail_fraction,
                      double ridge_strength, double noise, double jitter,
                      uint64_t seed, double* fit, uint8_t* ok, int nthreads);
 
+/* hillclimb.cpp:48-87 climb_random_first, batched: `walkers` descents from
+ * uniform starts, each with its own splitmix64 stream (seed, walker) -- the
+ * same draws, in the same order, as the device validator (tk_descents), so the
+ * per-rank arrival counts are bit-identical.  counts: N u32 (arrivals per
+ * end rank); evaluations: fitness lookups made.  Slots as build_slots
+ * (hillclimb.cpp:26-38); at most 256 slots. */
+int or_descents(uint32_t dims, const uint32_t* radix, const double* fit, int kind,
+                uint64_t walkers, uint64_t seed, int restart_scan, uint32_t* counts,
+                uint64_t* evaluations, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

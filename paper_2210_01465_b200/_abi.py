@@ -27,7 +27,7 @@ EXPORTS = [
     "tk_land_generate", "tk_land_copy_fitness", "tk_land_lookup", "tk_optimum",
     "tk_ffg_build", "tk_ffg_copy_out", "tk_census", "tk_pagerank",
     "tk_pagerank_copy_out", "tk_centrality", "tk_report_copy_out", "tk_analyze",
-    "tk_pagerank_csr", "tk_proportion_of_centrality",
+    "tk_pagerank_csr", "tk_proportion_of_centrality", "tk_descents",
     "tk_land_set_shard", "tk_land_replica_ptrs", "tk_land_set_peer_ptrs", "tk_land_ipc_handles",
     "tk_land_open_peers", "tk_shard_optimum", "tk_shard_pagerank_init", "tk_shard_pagerank_step",
     "tk_shard_pagerank_init_dev", "tk_shard_pagerank_step_dev", "tk_shard_pagerank_rewind",
@@ -84,6 +84,7 @@ def load(path: str = LIB_PATH):
         "tk_ffg_build": (I, [P, I, U64, I, PU64, PU64]),
         "tk_ffg_copy_out": (I, [P, P, P, P, P]),
         "tk_census": (I, [P, PU64, PU64, PU64, P]),
+        "tk_descents": (I, [P, C.c_uint64, C.c_uint64, I, P, PU64, PU64]),
         "tk_pagerank": (I, [P, D, D, C.c_int64, PI64, PD, PD]),
         "tk_pagerank_copy_out": (I, [P, P]),
         "tk_centrality": (I, [P, D, P, I, P]),

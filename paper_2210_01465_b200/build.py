@@ -16,7 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtk_landscape.so")
-SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_abi.cu"]
+SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_descent.cu",
+           "tk_abi.cu"]
 HEADERS = ["tk_internal.cuh", "tk_kernels.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -83,12 +84,15 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     from concurrent.futures import ThreadPoolExecutor
 
     objs, cmds = [], []
+    common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "tk_landscape.h")]
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", f"{'_' + variant if variant else ''}.o"))
+        objs.append(obj)
+        if not force and not _stale(obj, [os.path.join(CSRC, src), *common]):
+            continue  # translation unit unchanged since its object was built
         cmds.append([nvcc(), *flags((["-Xptxas", "-v"] if verbose else []) + VARIANTS[variant]),
                      "-c", os.path.join(CSRC, src), "-o", obj])
-        objs.append(obj)
-    with ThreadPoolExecutor(len(cmds)) as ex:  # translation units compile independently
+    with ThreadPoolExecutor(max(1, len(cmds))) as ex:  # translation units compile independently
         for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
             f.result()
     cmd = [nvcc(), *ARCH, "-ccbin", host_cxx(), "-shared", "-o", out, *objs]

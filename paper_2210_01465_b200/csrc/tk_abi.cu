@@ -889,8 +889,17 @@ int tk_land_lookup(tk_land* l, const uint64_t* keys, uint64_t n, double* fitness
     return TK_OK;
 }
 
+// Whole-space entry points refuse a sharded handle: its FFG rows, flags and
+// PageRank cover only its own key range (tk_shard_* are the per-shard calls).
+static int check_unsharded(const tk_land* l, const char* what) {
+    if (l->sharded)
+        return fail(TK_ESTATE, std::string(what) + ": sharded handle (use the tk_shard_* calls)");
+    return TK_OK;
+}
+
 int tk_optimum(tk_land* l, double* f_opt, uint64_t* rank) {
     if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "optimum")) return st;
     return do_optimum(l, f_opt, rank);
 }
 
@@ -910,6 +919,8 @@ int tk_ffg_copy_out(tk_land* l, uint64_t* offsets, uint32_t* targets, uint8_t* i
                     uint32_t* minima) {
     if (int st = check_land(l)) return st;
     if (!l->built) return fail(TK_ESTATE, "copy_out: build the FFG first");
+    if (offsets || targets || is_sink)
+        if (int st = check_unsharded(l, "ffg_copy_out")) return st;
     TKC(set_dev(l));
     if ((offsets || targets) && !l->emitted) {
         const bool pr = l->pr_done;
@@ -939,6 +950,7 @@ int tk_ffg_copy_out(tk_land* l, uint64_t* offsets, uint32_t* targets, uint8_t* i
 int tk_census(tk_land* l, uint64_t* fail_points, uint64_t* local_minima, uint64_t* interior,
               uint64_t* minima_ranks) {
     if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "census")) return st;
     if (!l->built) return fail(TK_ESTATE, "census: build the FFG first");
     TKC(set_dev(l));
     // strict minima (flag bit2) compacted in ascending rank with a look-back scan
@@ -965,6 +977,7 @@ int tk_census(tk_land* l, uint64_t* fail_points, uint64_t* local_minima, uint64_
 int tk_pagerank(tk_land* l, double damping, double tol, int64_t max_iter, int64_t* iterations,
                 double* residual, double* sum) {
     if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "pagerank")) return st;
     int st = do_pagerank(l, damping, tol, max_iter);
     if (iterations) *iterations = l->iterations;
     if (residual) *residual = l->residual;
@@ -984,6 +997,7 @@ int tk_pagerank_copy_out(tk_land* l, double* r) {
 
 int tk_centrality(tk_land* l, double f_opt, const double* p, int n_p, double* c_p) {
     if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "centrality")) return st;
     if (!p || !c_p) return fail(TK_EINVAL, "centrality: null buffer");
     return do_centrality(l, f_opt, p, n_p, c_p);
 }
@@ -1015,6 +1029,7 @@ int tk_report_copy_out(tk_land* l, double f_opt, uint64_t* ranks, double* fitnes
 int tk_analyze(tk_land* l, int kind, double damping, double tol, int64_t max_iter,
                uint64_t node_limit, int p_max_percent, int emit_csr, tk_report_summary* out) {
     if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "analyze")) return st;
     if (!out) return fail(TK_EINVAL, "analyze: null summary");
     if (p_max_percent < 0 || p_max_percent >= TK_MAX_CP)
         return fail(TK_EINVAL, "analyze: p_max_percent must be in [0, 100]");
@@ -1052,6 +1067,65 @@ int tk_analyze(tk_land* l, int kind, double damping, double tol, int64_t max_ite
     out->ms_ffg = l->ms_build;
     out->ms_pagerank = l->ms_pr;
     TKC(cudaEventElapsedTime(&out->ms_centrality, l->ev[4], l->ev[5]));
+    return TK_OK;
+    TK_GUARD_END
+}
+
+// ------------------------------------------------ random-walk validator --
+
+int tk_descents(tk_land* l, uint64_t walkers, uint64_t seed, int restart_scan,
+                uint64_t* arrivals, uint64_t* fail_arrivals, uint64_t* evaluations) {
+    if (int st = check_land(l)) return st;
+    if (int st = check_unsharded(l, "descents")) return st;
+    if (!l->built) return fail(TK_ESTATE, "descents: build the FFG first (neighbourhood, minima)");
+    TK_GUARD_BEGIN
+    TKC(set_dev(l));
+    tk::DescentArgs a{};
+    a.fit = l->fit.as<double>();
+    a.n = l->n;
+    a.dims = static_cast<int>(l->radix_in.size());
+    a.kind = l->kind;
+    a.restart_scan = restart_scan ? 1 : 0;
+    a.walkers = walkers;
+    a.seed = seed;
+    int S = 0;
+    for (int i = 0; i < a.dims; ++i) {  // build_slots (hillclimb.cpp:26-38)
+        a.radix[i] = l->radix_in[i];
+        a.stride[i] = l->strides_in[i];
+        const int m = static_cast<int>(l->radix_in[i]);
+        if (l->kind == TK_HAMMING) {
+            for (int alt = 0; alt + 1 < m; ++alt) {
+                if (S == tk::kMaxDescentSlots) return fail(TK_EINVAL, "descents: more than 256 slots");
+                a.slot_dim[S] = static_cast<uint8_t>(i);
+                a.slot_alt[S++] = static_cast<int16_t>(alt);
+            }
+        } else if (m > 1) {
+            if (S + 2 > tk::kMaxDescentSlots) return fail(TK_EINVAL, "descents: more than 256 slots");
+            a.slot_dim[S] = static_cast<uint8_t>(i);
+            a.slot_alt[S++] = -1;
+            a.slot_dim[S] = static_cast<uint8_t>(i);
+            a.slot_alt[S++] = 1;
+        }
+    }
+    a.slots = S;
+    const uint64_t m = l->n_minima;
+    TKC(ensure(l->tmp, l->n * 4 + 16 + m * 8));
+    a.counts = l->tmp.as<uint32_t>();
+    a.evaluations = reinterpret_cast<unsigned long long*>(l->tmp.as<uint8_t>() + ((l->n * 4 + 7) & ~7ull));
+    unsigned long long* dout = a.evaluations + 1;
+    TKC(cudaMemsetAsync(l->tmp.p, 0, ((l->n * 4 + 7) & ~7ull) + 8, l->stream));
+    if (walkers) TKC(tk::launch_descents(a, l->num_sms, l->stream));
+    TKC(tk::launch_gather_counts(l->minima.as<uint32_t>(), m, a.counts, dout, l->stream));
+    std::vector<unsigned long long> h(m);
+    unsigned long long ev = 0;
+    if (m) TKC(cudaMemcpyAsync(h.data(), dout, m * 8, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaMemcpyAsync(&ev, a.evaluations, 8, cudaMemcpyDeviceToHost, l->stream));
+    TKC(cudaStreamSynchronize(l->stream));
+    uint64_t at_minima = 0;
+    for (uint64_t k = 0; k < m; ++k) at_minima += h[k];
+    if (arrivals && m) std::memcpy(arrivals, h.data(), m * 8);
+    if (fail_arrivals) *fail_arrivals = walkers - at_minima;
+    if (evaluations) *evaluations = ev;
     return TK_OK;
     TK_GUARD_END
 }

@@ -262,4 +262,25 @@ cudaError_t launch_report(const uint32_t* minima, uint64_t m, const double* fit,
 cudaError_t launch_gather_values(const uint32_t* idx, uint64_t m, const double* src,
                                  double* dst, cudaStream_t stream);
 
+// ---- random-walk validator (tk_descent.cu) ------------------------------------
+constexpr int kMaxDescentSlots = 256;
+struct DescentArgs {
+    const double* fit;                 // rank-indexed fitness (failed = kFailFitness)
+    unsigned long long n;              // nodes
+    int dims;                          // the space's own dims (radix-1 dims included)
+    int kind;                          // TK_HAMMING / TK_ADJACENT
+    int slots;                         // build_slots size (<= kMaxDescentSlots)
+    int restart_scan;
+    unsigned long long walkers, seed;
+    uint32_t radix[kMaxDims];
+    unsigned long long stride[kMaxDims];
+    uint8_t slot_dim[kMaxDescentSlots];
+    int16_t slot_alt[kMaxDescentSlots];
+    uint32_t* counts;                  // N arrivals per end rank (zeroed by the caller)
+    unsigned long long* evaluations;   // fitness lookups (zeroed by the caller)
+};
+cudaError_t launch_descents(const DescentArgs& a, int num_sms, cudaStream_t stream);
+cudaError_t launch_gather_counts(const uint32_t* idx, uint64_t m, const uint32_t* counts,
+                                 unsigned long long* out, cudaStream_t stream);
+
 }  // namespace tk

@@ -317,6 +317,18 @@ class Landscape:
             _check(self.L.tk_census(self.h, C.byref(fp), C.byref(lm), C.byref(it), _ptr(ranks)))
         return PointCensus(self.kind, self.n, fp.value, lm.value, it.value, ranks)
 
+    # ---- random-walk validator
+    def descents(self, walkers: int, seed: int = 0, restart_scan: bool = True):
+        """hillclimb.cpp:48-87 climb_random_first from `walkers` uniform starts,
+        on the device (tk_descents), in the neighbourhood of the last build.
+        Returns (arrivals per FFG minimum in ffg minima order, arrivals at
+        failed sinks, fitness evaluations)."""
+        arr = np.zeros(self.n_minima, np.uint64)
+        fail, ev = C.c_uint64(), C.c_uint64()
+        _check(self.L.tk_descents(self.h, walkers, seed, int(restart_scan),
+                                  _ptr(arr) if arr.size else None, C.byref(fail), C.byref(ev)))
+        return arr, fail.value, ev.value
+
     # ---- PageRank / C_p
     def pagerank(self, damping=0.85, tol=1e-10, max_iter=100000):
         it, res, s = C.c_int64(), C.c_double(), C.c_double()

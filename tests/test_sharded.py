@@ -401,3 +401,28 @@ def test_two_process_gloo(kind):
     for r in (0, 1):
         check(results[r], ref, fit, ok, kind)
     assert results[0] == results[1]
+
+
+@pytest.mark.gpu
+def test_whole_space_calls_refuse_a_sharded_handle():
+    """A sharded handle holds only its key range: the whole-space entry points
+    return TK_ESTATE instead of shard-local or uninitialised data (tk_landscape.h
+    key-range sharding section)."""
+    import torch
+
+    import paper_2210_01465_b200 as tk
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    radix = [8, 8, 6, 6, 4]
+    n = O.space_size(radix)
+    fit, ok = O.gen_iid(n, 0.2, 7)
+    s = S.GpuShard(radix, 0, 2, device=0)
+    s.land.load_dense(fit, ok)
+    s.build(O.ADJACENT)
+    for call in (lambda: s.land.optimum(), lambda: s.land.ffg_arrays(), lambda: s.land.census(),
+                 lambda: s.land.pagerank(), lambda: s.land.centrality(1.0, [0.0]),
+                 lambda: s.land.analyze(O.ADJACENT)):
+        with pytest.raises(tk.Error, match="sharded handle"):
+            call()
+    s.land.close()
