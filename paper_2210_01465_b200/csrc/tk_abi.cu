@@ -105,6 +105,7 @@ struct tk_land {
 
     DevBuf fit, ok;
     bool loaded = false;
+    bool fit_clean = false;  // every fitness finite and none -0 (FFG count fast compares)
     DevBuf hkeys, hvals, staging_keys, staging_vals, staging_cfg, claimed;
     uint64_t hcap = 0;  // 0 = no valid-set hash table for the loaded table yet
 
@@ -267,6 +268,7 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     tk::StagePlan plan{};
     if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
         tk::make_stage_plan(s, false, stage_budget(l), &plan)) {
+        plan.fast = l->fit_clean && !std::getenv("TK_FFG_SLOW") ? 1 : 0;
         // T-rank tiles over the whole space, or over this handle's shard
         const uint64_t lo = l->sharded ? l->shard_lo : 0, hi = l->sharded ? l->shard_hi : n;
         const uint32_t nt = static_cast<uint32_t>((hi - lo + plan.T - 1) / plan.T);
@@ -579,6 +581,7 @@ int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const doubl
                                "points (cache.hpp:15)");
     if (err & 2) return fail(TK_EINVAL, "load: duplicate configuration key");
     l->loaded = true;
+    l->fit_clean = !(err & 16);
     return TK_OK;
 }
 
@@ -774,6 +777,7 @@ int tk_land_load_dense(tk_land* l, const double* fitness, const uint8_t* ok, int
     l->opt_ready = false;
     l->built = l->pr_done = false;
     l->loaded = !(l->hsmall->err & 4);
+    l->fit_clean = !(l->hsmall->err & 16);
     if (!l->loaded)
         return fail(TK_EINVAL, "load_dense: an ok mean >= kFailFitness (1e10) would order above "
                                "failed points (cache.hpp:15)");
@@ -848,6 +852,7 @@ int tk_land_generate(tk_land* l, int gen, double fail_fraction, uint64_t seed) {
     TKC(cudaStreamSynchronize(l->stream));
     l->hcap = 0;
     l->loaded = true;
+    l->fit_clean = true;  // 1 + u or 1 / (1 - u), u in [0, 1), and kFailFitness: finite, > 0
     l->opt_ready = false;
     l->built = l->pr_done = false;
     return TK_OK;

@@ -130,8 +130,16 @@ __global__ void fill_failed_kernel(uint32_t n, double* __restrict__ fit) {
         fit[u] = kFailFitness;
 }
 
+// A fitness the FFG count kernel's sign-of-difference compares cannot take:
+// not finite (NaN, +-inf) or -0 (tk_land::fit_clean, err bit 16).
+__device__ __forceinline__ bool unclean(double f) {
+    const unsigned long long b = __double_as_longlong(f);
+    return ((b >> 52) & 0x7ff) == 0x7ff || b == 0x8000000000000000ull;
+}
+
 // err bits: 1 key outside the space, 2 duplicate key, 4 mean >= kFailFitness
-// (decision A11: an ok mean must order below every failed point)
+// (decision A11: an ok mean must order below every failed point), 16 a mean
+// that is not finite or is -0 (unclean)
 __global__ void valid_scatter_kernel(const unsigned long long* __restrict__ keys,
                                      const double* __restrict__ vals, uint64_t nv, uint64_t n,
                                      double* __restrict__ fit, uint8_t* __restrict__ ok,
@@ -145,6 +153,7 @@ __global__ void valid_scatter_kernel(const unsigned long long* __restrict__ keys
             continue;
         }
         if (v >= kFailFitness) atomicOr(err, 4);
+        if (unclean(v)) atomicOr(err, 16);
         const unsigned int bit = 1u << (k & 31);
         const unsigned int old = atomicOr(claimed + (k >> 5), bit);
         if (old & bit) {
@@ -160,14 +169,19 @@ __global__ void valid_scatter_kernel(const unsigned long long* __restrict__ keys
 // set_failed) and an ok mean >= kFailFitness is rejected (A11).
 __global__ void normalize_dense_kernel(uint32_t n, double* __restrict__ fit,
                                        const uint8_t* __restrict__ ok, int* err) {
-    bool bad = false;
+    bool bad = false, dirty = false;
     for (uint64_t u = grid_stride_begin<uint64_t>(); u < n;
          u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const double f = fit[u];
-        if (ok[u]) bad |= f >= kFailFitness;
-        else if (!(f == kFailFitness)) fit[u] = kFailFitness;
+        if (ok[u]) {
+            bad |= f >= kFailFitness;
+            dirty |= unclean(f);
+        } else if (!(f == kFailFitness)) {
+            fit[u] = kFailFitness;
+        }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 4);
+    if (__any_sync(0xffffffffu, dirty) && (threadIdx.x & 31) == 0) atomicOr(err, 16);
 }
 
 __global__ void count_ok_kernel(const uint8_t* __restrict__ ok, uint32_t n,

@@ -181,6 +181,7 @@ struct StagePlan {
     unsigned int dim_inv, dim_uni, dim_tile;
     unsigned long long npad2;  // f64 arrays hold at least this many elements (even)
     unsigned long long npad16; // u8/u32 arrays are padded to this many elements
+    int fast;                  // FFG count: table is clean (finite, no -0): DADD-sign compares
 };
 // kind_pr: PageRank layout (u32 pw[T], f64 r[T], window) vs FFG (u8 ok[T], window)
 // stage_r: PageRank stages the old ranks too (the sharded step); the single-GPU
