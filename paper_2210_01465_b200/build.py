@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtk_landscape.so")
 SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_descent.cu",
            "tk_abi.cu"]
-HEADERS = ["tk_internal.cuh", "tk_kernels.cuh"]
+HEADERS = ["tk_internal.cuh", "tk_kernels.cuh", "tk_pipe.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

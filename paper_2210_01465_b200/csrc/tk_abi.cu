@@ -128,7 +128,8 @@ struct tk_land {
     cudaEvent_t ev[6] = {};
     float ms_build = 0.f, ms_pr = 0.f;  // kernel-only device time of the last launch
     bool staged = false;                // last build used the TMA-staged kernel
-    int pr_staged = 0;                  // last PageRank kernel: 0 per-lane, 1 staged, 2 row-tiled
+    int pr_staged = 0;  // last PageRank kernel: 0 per-lane, 1 staged, 2 row-tiled,
+                        // 3 Hamming staged, 4 Hamming tiled
     int pr_grid = 0;
     bool opt_ready = false;  // small->f_opt/rank/has hold f_opt of the loaded table
 
@@ -428,7 +429,8 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                  tk::PrArgs a, DevBuf& part, Small* ds, Small* hs, cudaStream_t stream,
                  double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
                  cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr,
-                 const tk::StagePlan* plan = nullptr, const tk::RowPlan* rplan = nullptr) {
+                 const tk::StagePlan* plan = nullptr, const tk::RowPlan* rplan = nullptr,
+                 int smem_budget = 0, int* kernel_used = nullptr) {
     const int maxg = (plan || rplan) ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
     TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
@@ -453,15 +455,22 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                           : plan ? static_cast<int>(std::min<uint64_t>(
                                      num_sms, (static_cast<uint64_t>(a.n) + plan->T - 1) / plan->T))
                                : num_sms;
-    const bool ham_tiled = !plan && mode == tk::MODE_HAM && staged_enabled() &&
+    tk::HamStagePlanOut hplan{};
+    const bool ham_staged = !plan && !rplan && mode == tk::MODE_HAM && staged_enabled() &&
+                            smem_budget > 0 && tk::ham_staged_plan(s, smem_budget, &hplan);
+    const bool ham_tiled = !plan && !ham_staged && mode == tk::MODE_HAM && staged_enabled() &&
                            tk::ham_tiled_supported(s);
-    TKC(gated_coop_launch(device, num_sms, ham_tiled ? num_sms : footprint, stream, [&] {
+    TKC(gated_coop_launch(device, num_sms, (ham_tiled || ham_staged) ? num_sms : footprint, stream, [&] {
         if (rplan) return tk::launch_pagerank_rows(s, *rplan, a, num_sms, &g, stream);
         if (plan) return tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream);
+        if (ham_staged)
+            return tk::launch_pagerank_ham_staged(s, wide, hplan, a, num_sms, &g, stream);
         if (ham_tiled) return tk::launch_pagerank_ham_tiled(s, wide, a, num_sms, &g, stream);
         return tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
     }));
     if (e1) TKC(cudaEventRecord(e1, stream));
+    // 0 per-lane, 1 staged (Adjacent), 2 row-tiled, 3 Hamming staged, 4 Hamming tiled
+    if (kernel_used) *kernel_used = rplan ? 2 : plan ? 1 : ham_staged ? 3 : ham_tiled ? 4 : 0;
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
     TKC(cudaStreamSynchronize(stream));
     if (e0 && e1 && ms) TKC(cudaEventElapsedTime(ms, e0, e1));
@@ -499,7 +508,7 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
                       l->small.as<Small>(), l->hsmall, l->stream, d, tol, max_iter, l->ev[2],
                       l->ev[3], &l->ms_pr, &l->pr_grid, have_plan ? &plan : nullptr,
-                      have_rows ? &rplan : nullptr);
+                      have_rows ? &rplan : nullptr, stage_budget(l), &l->pr_staged);
     if (st) return st;
     const PrOut& o = l->hsmall->pr;
     l->iterations = o.iter;

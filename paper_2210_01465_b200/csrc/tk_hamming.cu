@@ -33,6 +33,7 @@
 #include <cstdlib>
 
 #include "tk_kernels.cuh"
+#include "tk_pipe.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -234,6 +235,317 @@ __global__ void __launch_bounds__(kHT, TK_HAM_MINB)
     }
 }
 
+// ================================================== staged Hamming kernel --
+//
+// The tiled kernel above gathers every line value with a warp load and keeps
+// only two loads in flight per thread: it is bound by memory-level parallelism
+// (DRAM at ~20 %) and, sweeping in rank order, re-reads the lines of the
+// slowest dimensions from DRAM (~190 B per rank and iteration on C5).
+//
+// This kernel streams the lines through shared memory instead.  The dims split
+// into OUTER dims 0..k-1, whose strides are multiples of the tile (their digit
+// is fixed over a tile), and INNER dims k..D-1, whose lines stay inside the
+// aligned block of B = s_{k-1} ranks that holds the tile.  For a tile at v0:
+//   - every outer neighbour line (i, j) is one whole range c[v0 + (j - x_i) s_i,
+//     + T): producer warps copy the ranges with 1-D bulk copies (TMA) into a
+//     ring of T-double slots, one mbarrier pair per slot, in exactly the order
+//     the in-edge sum consumes them;
+//   - the inner lines come from a copy of the block (double-buffered).
+// The in-edge sum keeps the oracle's order (ascending source rank): lower
+// ranges dims 0..k-1, inner lower / upper from the block, upper ranges dims
+// k-1..0 -- so r' stays bit-identical.
+//
+// Tiles are swept with the block offset fastest, then x_0, x_1, ... x_{k-1}:
+// the concurrently processed tiles of the grid share their outer lines, so
+// each line is read from DRAM once per sweep and re-read from L2 by its
+// siblings (the rank-order sweep of the tiled kernel misses L2 on dims 0-1).
+constexpr int kHsT = 512;                      // ranks per tile = consumer threads
+constexpr int kHsConsumerWarps = kHsT / 32;
+constexpr int kHsProdWarps = 4;
+constexpr int kHsThreads = kHsT + 32 * kHsProdWarps;
+constexpr int kHsMaxSlots = 48;
+constexpr int kHsMaxNear = 4096;               // block values (32 KB per buffer)
+
+struct HamStagePlan {
+    int k;                                  // outer dims
+    uint32_t B;                             // block = s_{k-1} ranks
+    uint32_t tpb;                           // tiles per block = B / T
+    int slots;                              // ring slots
+    unsigned long long tpb_magic;           // fdiv by tpb (0 when tpb == 1)
+    unsigned long long rmagic[kMaxDims];    // fdiv by radix[i]
+};
+
+struct HamPipe {
+    uint64_t full[kHsMaxSlots];
+    uint64_t empty[kHsMaxSlots];
+    uint64_t nfull[2];
+    uint64_t nempty[2];
+};
+
+// sweep position g -> tile origin v0 and the outer digits (block offset
+// fastest, then x_0 .. x_{k-1})
+template <int DIMS>
+__device__ __forceinline__ uint32_t ham_tile_of(const DevShape& s, const HamStagePlan& hp,
+                                                uint32_t g, uint32_t (&x)[DIMS],
+                                                uint32_t& w) {
+    const uint32_t r0 = fdiv(g, hp.tpb_magic);
+    w = g - r0 * hp.tpb;
+    uint32_t r = r0, v0 = w * kHsT;
+#pragma unroll
+    for (int i = 0; i < DIMS; ++i) {
+        if (i < hp.k) {
+            const uint32_t q = fdiv(r, hp.rmagic[i]);
+            x[i] = r - q * s.radix[i];
+            r = q;
+            v0 += x[i] * s.stride[i];
+        }
+    }
+    return v0;
+}
+
+template <int DIMS, typename MW>
+__global__ void __launch_bounds__(kHsThreads, 1)
+    pagerank_ham_staged_kernel(const __grid_constant__ DevShape s,
+                               const __grid_constant__ HamStagePlan hp, const PrArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ HamPipe pp;
+    __shared__ double s_red[kHsThreads / 32];
+    __shared__ double s_rcp[kMaxHamDeg + 1];
+    cg::grid_group grid = cg::this_grid();
+    const int t = threadIdx.x;
+    const uint32_t G = gridDim.x;
+    const uint32_t ntiles = a.n / kHsT;  // outer dims exist: T divides N
+    const int R = hp.slots;
+    const MW* __restrict__ inm = static_cast<const MW*>(a.inm);
+    double* ring = reinterpret_cast<double*>(smem);
+    double* nearb = ring + static_cast<size_t>(R) * kHsT;
+    if (t <= kMaxHamDeg) s_rcp[t] = t ? __drcp_rn(t) : 0.0;
+    if (t == 0) {
+        for (int i = 0; i < R; ++i) {
+            mbar_init(&pp.full[i], 1);
+            mbar_init(&pp.empty[i], kHsConsumerWarps);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&pp.nfull[i], 1);
+            mbar_init(&pp.nempty[i], kHsConsumerWarps);
+        }
+        fence_async_smem();
+    }
+
+    // r_0 = 1/N: c_0 = r_0 / outdeg (r_0 for sinks), D_0 = sum over sinks
+    double dang = 0.0;
+    const uint64_t gsize = static_cast<uint64_t>(G) * kHsThreads;
+    for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * kHsThreads + t; v < a.n; v += gsize) {
+        const uint32_t deg = __ldg(a.odeg + v);
+        if (deg) {
+            a.c0[v] = __ddiv_rn(a.inv_n, static_cast<double>(deg));
+        } else {
+            a.c0[v] = a.inv_n;
+            dang = __dadd_rn(dang, a.inv_n);
+        }
+    }
+    dang = block_sum<kHsThreads>(dang, s_red);
+    if (t == 0) a.part[blockIdx.x * 3 + 1] = dang;
+    fence_async_all();
+    grid.sync();
+    double D;
+    {
+        double acc = 0.0;
+        for (uint32_t b = t; b < G; b += kHsThreads) acc = __dadd_rn(acc, a.part[b * 3 + 1]);
+        D = block_sum<kHsThreads>(acc, s_red);
+    }
+
+    // ring / block pipeline position (continues across sweeps on both sides)
+    int slot = 0;
+    uint32_t sph = 0;       // phase of the current ring slot
+    uint32_t uses = 0;      // ring uses so far (producer: skip the first-round waits)
+    uint32_t ntile = 0;     // tiles so far (block buffer = ntile & 1, phase = (ntile >> 1) & 1)
+    auto advance = [&]() {
+        ++uses;
+        if (++slot == R) {
+            slot = 0;
+            sph ^= 1u;
+        }
+    };
+
+    auto sweep = [&](const double* cc, double dn, double* out, bool final_pass, double& lres,
+                     double& ldang, double& lsum) {
+        if (t >= kHsT) {  // ------------------------------------------ producers
+            const int pw = (t - kHsT) >> 5;
+            const bool leader = (t & 31) == 0;
+            for (uint32_t g = blockIdx.x; g < ntiles; g += G, ++ntile) {
+                uint32_t x[DIMS], w;
+                const uint32_t v0 = ham_tile_of<DIMS>(s, hp, g, x, w);
+                if (pw == 0 && leader) {
+                    const int nb = ntile & 1;
+                    if (ntile >= 2) mbar_wait(&pp.nempty[nb], ((ntile >> 1) & 1u) ^ 1u);
+                    mbar_expect_tx(&pp.nfull[nb], hp.B * 8);
+                    bulk_g2s(nearb + static_cast<size_t>(nb) * hp.B, cc + (v0 - w * kHsT),
+                             hp.B * 8, &pp.nfull[nb]);
+                }
+                // ranges in consumption order; range q of the stream goes to warp q % P
+                auto issue = [&](int i, uint32_t j) {
+                    if (static_cast<int>(uses % kHsProdWarps) == pw && leader) {
+                        if (uses >= static_cast<uint32_t>(R)) mbar_wait(&pp.empty[slot], sph ^ 1u);
+                        mbar_expect_tx(&pp.full[slot], kHsT * 8);
+                        const double* src = cc + (v0 + (j - x[i]) * s.stride[i]);
+                        bulk_g2s(ring + static_cast<size_t>(slot) * kHsT, src, kHsT * 8,
+                                 &pp.full[slot]);
+                    }
+                    advance();
+                };
+                for (int i = 0; i < hp.k; ++i)
+                    for (uint32_t j = 0; j < x[i]; ++j) issue(i, j);
+                for (int i = hp.k - 1; i >= 0; --i)
+                    for (uint32_t j = x[i] + 1; j < s.radix[i]; ++j) issue(i, j);
+            }
+            return;
+        }
+        // ------------------------------------------------------- consumers
+        const int lane = t & 31;
+        for (uint32_t g = blockIdx.x; g < ntiles; g += G, ++ntile) {
+            uint32_t x[DIMS], w;
+            const uint32_t v0 = ham_tile_of<DIMS>(s, hp, g, x, w);
+            const uint32_t v = v0 + t;
+            const uint32_t o = w * kHsT + t;  // offset in the block
+#pragma unroll
+            for (int i = 0; i < DIMS; ++i)
+                if (i >= hp.k) {
+                    const uint32_t q = fdiv(o, s.magic[i]);
+                    x[i] = q - fdiv(q, hp.rmagic[i]) * s.radix[i];
+                }
+            const unsigned long long mask = static_cast<unsigned long long>(__ldcs(inm + v));
+            const uint32_t deg = __ldcs(a.odeg + v);
+            double acc = 0.0;
+            auto take = [&](int bit) {
+                mbar_wait(&pp.full[slot], sph);
+                const double val = ring[static_cast<size_t>(slot) * kHsT + t];
+                if ((mask >> bit) & 1ull) acc = __dadd_rn(acc, val);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pp.empty[slot]);
+                advance();
+            };
+            // lower neighbours of the outer dims (dims ascending, values ascending)
+            for (int i = 0; i < hp.k; ++i)
+                for (uint32_t j = 0; j < x[i]; ++j) take(s.base[i] + static_cast<int>(j));
+            // inner dims from the block copy
+            const int nb = ntile & 1;
+            mbar_wait(&pp.nfull[nb], (ntile >> 1) & 1u);
+            const double* blk = nearb + static_cast<size_t>(nb) * hp.B + o;
+#pragma unroll
+            for (int i = 0; i < DIMS; ++i) {
+                if (i < hp.k) continue;
+                const uint32_t st = s.stride[i], xi = x[i];
+                const double* row = blk - static_cast<int>(xi * st);
+                const unsigned long long mi = mask >> s.base[i];
+#pragma unroll kHamUnroll
+                for (uint32_t j = 0; j < xi; ++j)
+                    if ((mi >> j) & 1ull) acc = __dadd_rn(acc, row[j * st]);
+            }
+            const double cold = final_pass ? 0.0 : blk[0];
+#pragma unroll
+            for (int ii = 0; ii < DIMS; ++ii) {
+                const int i = DIMS - 1 - ii;
+                if (i < hp.k) continue;
+                const uint32_t st = s.stride[i], xi = x[i], m = s.radix[i];
+                const double* row = blk - static_cast<int>(xi * st);
+                const unsigned long long mi = mask >> (s.base[i] + xi);
+#pragma unroll kHamUnroll
+                for (uint32_t j = xi + 1; j < m; ++j)
+                    if ((mi >> (j - xi - 1)) & 1ull) acc = __dadd_rn(acc, row[j * st]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pp.nempty[nb]);
+            // upper neighbours of the outer dims (dims descending, values ascending)
+            for (int i = hp.k - 1; i >= 0; --i)
+                for (uint32_t j = x[i] + 1; j < s.radix[i]; ++j)
+                    take(s.base[i] + static_cast<int>(j) - 1);
+            const double xr = __dadd_rn(a.teleport, __dmul_rn(a.damping, __dadd_rn(acc, dn)));
+            if (final_pass) {
+                out[v] = xr;
+                continue;
+            }
+            double q, d;
+            if (deg) {
+                const double dd = static_cast<double>(deg);
+                q = div_small_h(xr, dd, s_rcp[deg]);
+                d = fabs(__fma_rn(cold, dd, -xr));
+            } else {
+                q = xr;
+                d = fabs(__dsub_rn(xr, cold));
+                ldang = __dadd_rn(ldang, xr);
+            }
+            lres = __dadd_rn(lres, d);
+            lsum = __dadd_rn(lsum, xr);
+            __stcs(out + v, q);
+        }
+    };
+
+    int cur = 0;
+    long long it = 0;
+    double res = 0.0, sum = 0.0, dn_last = 0.0;
+    int status = 1;
+    while (it < a.max_iter) {
+        const double dn = __ddiv_rn(D, a.nd);
+        const double* cc = cur ? a.c1 : a.c0;
+        double* cn = cur ? a.c0 : a.c1;
+        double lres = 0.0, ldang = 0.0, lsum = 0.0;
+        sweep(cc, dn, cn, false, lres, ldang, lsum);
+        fence_async_all();  // this sweep's stores before the next sweep's bulk reads
+        lres = block_sum<kHsThreads>(lres, s_red);
+        ldang = block_sum<kHsThreads>(ldang, s_red);
+        lsum = block_sum<kHsThreads>(lsum, s_red);
+        double* part = a.part + static_cast<size_t>((it + 1) & 1) * G * 3;
+        if (t == 0) {
+            part[blockIdx.x * 3 + 0] = lres;
+            part[blockIdx.x * 3 + 1] = ldang;
+            part[blockIdx.x * 3 + 2] = lsum;
+        }
+        grid.sync();
+        double r3[3] = {0.0, 0.0, 0.0};
+        for (uint32_t b = t; b < G; b += kHsThreads)
+            for (int k3 = 0; k3 < 3; ++k3) r3[k3] = __dadd_rn(r3[k3], part[b * 3 + k3]);
+        res = block_sum<kHsThreads>(r3[0], s_red);
+        D = block_sum<kHsThreads>(r3[1], s_red);
+        sum = block_sum<kHsThreads>(r3[2], s_red);
+        dn_last = dn;
+        ++it;
+        cur ^= 1;
+        if (res < a.tol) {
+            status = 0;
+            break;
+        }
+    }
+    {
+        double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+        sweep(cur ? a.c0 : a.c1, dn_last, a.r0, true, l0, l1, l2);
+    }
+    if (blockIdx.x == 0 && t == 0) {
+        *a.out_iter = it;
+        *a.out_res = res;
+        *a.out_sum = sum;
+        *a.out_parity = 0;
+        *a.out_status = status;
+    }
+}
+
+template <typename MW>
+void* ham_staged_kernel(int dims) {
+    switch (dims) {
+#define TK_HAM_CASE(D) \
+    case D: return reinterpret_cast<void*>(pagerank_ham_staged_kernel<D, MW>);
+        TK_HAM_CASE(2) TK_HAM_CASE(3) TK_HAM_CASE(4) TK_HAM_CASE(5) TK_HAM_CASE(6)
+        TK_HAM_CASE(7) TK_HAM_CASE(8) TK_HAM_CASE(9) TK_HAM_CASE(10) TK_HAM_CASE(11)
+        TK_HAM_CASE(12) TK_HAM_CASE(13) TK_HAM_CASE(14) TK_HAM_CASE(15) TK_HAM_CASE(16)
+#undef TK_HAM_CASE
+        default: return nullptr;
+    }
+}
+
+unsigned long long magic_of(uint32_t d) {
+    return d <= 1 ? 0ull : (~0ull) / d + 1ull;  // ceil(2^64 / d) for d >= 2
+}
+
 template <typename MW>
 void* ham_kernel(int dims) {
     switch (dims) {
@@ -249,6 +561,62 @@ void* ham_kernel(int dims) {
 }
 
 }  // namespace
+
+// Shapes the staged kernel takes: k >= 1 outer dims (strides multiples of the
+// tile), a block B = s_{k-1} of at most kHsMaxNear ranks, at least one inner
+// dim, and slots <= 64 (u64 in-mask).
+bool ham_staged_plan(const DevShape& s, int smem_budget, HamStagePlanOut* out) {
+    if (s.kind != TK_HAMMING || s.dims < 2 || s.dims > 16 || s.slots > kMaxHamDeg) return false;
+    if (std::getenv("TK_HAM_TILED")) return false;  // A/B: keep the tiled kernel
+    int k = 0;
+    while (k < s.dims && s.stride[k] >= static_cast<uint32_t>(kHsT)) ++k;
+    if (k == 0 || k == s.dims) return false;
+    for (int i = 0; i < k; ++i)
+        if (s.stride[i] % kHsT) return false;
+    const uint32_t B = s.stride[k - 1];
+    if (B > static_cast<uint32_t>(kHsMaxNear)) return false;
+    const long long ring_bytes = smem_budget - 2ll * B * 8 - 256;
+    int slots = static_cast<int>(ring_bytes / (kHsT * 8));
+    if (slots > kHsMaxSlots) slots = kHsMaxSlots;
+    if (slots < 4) return false;
+    out->k = k;
+    out->B = B;
+    out->slots = slots;
+    return true;
+}
+
+cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamStagePlanOut& po,
+                                       const PrArgs& a, int num_sms, int* grid_out,
+                                       cudaStream_t stream) {
+    HamStagePlan hp{};
+    hp.k = po.k;
+    hp.B = po.B;
+    hp.tpb = po.B / kHsT;
+    hp.slots = po.slots;
+    hp.tpb_magic = magic_of(hp.tpb);
+    for (int i = 0; i < s.dims; ++i) hp.rmagic[i] = magic_of(s.radix[i]);
+    void* k = wide ? ham_staged_kernel<unsigned long long>(s.dims) : ham_staged_kernel<uint32_t>(s.dims);
+    if (!k) return cudaErrorInvalidValue;
+    const int smem = po.slots * kHsT * 8 + 2 * static_cast<int>(po.B) * 8;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int bps = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, kHsThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (bps < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t ntiles = static_cast<uint64_t>(a.n) / kHsT;
+    uint64_t g = static_cast<uint64_t>(num_sms);
+    if (g > ntiles) g = ntiles;
+    *grid_out = static_cast<int>(g);
+    if (std::getenv("TK_DEBUG"))
+        std::fprintf(stderr, "[tk] pagerank_ham_staged k=%d B=%u slots=%d grid=%llu smem=%d\n",
+                     hp.k, hp.B, hp.slots, static_cast<unsigned long long>(g), smem);
+    DevShape sc = s;
+    PrArgs ac = a;
+    void* args[] = {&sc, &hp, &ac};
+    return cudaLaunchCooperativeKernel(k, dim3(static_cast<unsigned>(g)), dim3(kHsThreads), args,
+                                       static_cast<size_t>(smem), stream);
+}
 
 bool ham_tiled_supported(const DevShape& s) {
     if (s.kind != TK_HAMMING || s.dims < 1 || s.dims > 16 || s.slots > kMaxHamDeg) return false;

@@ -145,6 +145,17 @@ int pagerank_max_grid(int mode, bool wide, int num_sms);
 // Hamming: tiled contribution-only kernel (tk_hamming.cu) for shapes whose
 // digits align with 512-rank tiles; cudaErrorNotSupported otherwise
 bool ham_tiled_supported(const DevShape& s);
+// Hamming: staged kernel (tk_hamming.cu) -- outer lines streamed through a
+// shared-memory ring with TMA bulk copies, inner lines from a block copy
+struct HamStagePlanOut {
+    int k;        // outer dims
+    uint32_t B;   // block ranks (s_{k-1})
+    int slots;    // ring slots of 512 doubles
+};
+bool ham_staged_plan(const DevShape& s, int smem_budget, HamStagePlanOut* out);
+cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamStagePlanOut& p,
+                                       const PrArgs& a, int num_sms, int* grid_out,
+                                       cudaStream_t stream);
 cudaError_t launch_pagerank_ham_tiled(const DevShape& s, bool wide, const PrArgs& a, int num_sms,
                                       int* grid_out, cudaStream_t stream);
 

@@ -236,7 +236,8 @@ class Landscape:
         _check(self.L.tk_land_kernel_info(self.h, C.byref(sb), C.byref(sp), C.byref(g),
                                           C.byref(mb), C.byref(mp)))
         return dict(staged_build=bool(sb.value), staged_pagerank=sp.value > 0,
-                    pagerank_kernel={2: "rows", 1: "staged"}.get(sp.value, "per-lane"),
+                    pagerank_kernel={1: "staged", 2: "rows", 3: "ham_staged",
+                                     4: "ham_tiled"}.get(sp.value, "per-lane"),
                     pagerank_grid=g.value, ms_build=mb.value, ms_pagerank=mp.value)
 
     # ---- ingestion

@@ -296,18 +296,26 @@ def test_row_tiled_pagerank_matches_oracle(tk, monkeypatch, rows, radix, q):
         assert abs(s.c_p[k] - c) <= CP_ATOL
 
 
-@pytest.mark.parametrize("path", ["tiled", "v1"])
+@pytest.mark.parametrize("path", ["staged", "tiled", "v1"])
 @pytest.mark.parametrize("radix,q", [
     ([6, 6, 4, 4, 4, 4, 2, 2], 0.2),       # uniform / tile-aligned / per-thread digits
     ([8, 4, 4, 4, 2, 2, 4], 0.0),          # N = 8192, one uniform dim
     ([8, 8, 8, 4, 4, 4, 4, 2, 2], 0.1),    # 35 Hamming slots: u64 in-masks
     ([4, 4, 4, 4, 2], 0.3),                # N = 512: one tile, all digits per thread
+    ([7, 5, 3, 4, 4, 4, 2, 2, 2], 0.15),   # odd outer radices, block of 512 (one tile)
+    ([3, 5, 8, 4, 4, 4, 2, 2], 0.05),      # block of 2048 ranks (4 tiles per block)
+    ([5, 3, 16, 4, 4, 4, 2, 2], 0.4),      # block of 4096 (8 tiles), 40 % failed
+    ([2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2], 0.1),  # 5 outer binary dims
 ])
 def test_hamming_tiled_pagerank_matches_oracle(tk, monkeypatch, path, radix, q):
-    """The tiled Hamming kernel (tk_hamming.cu) and the per-lane one agree with
-    the oracle: same iteration count, rank vector within 1e-12, C_p within 1e-9."""
+    """The Hamming kernels (tk_hamming.cu: staged -- outer lines through a TMA
+    ring, inner lines from a block copy -- and tiled) and the per-lane one agree
+    with the oracle: same iteration count, rank vector within 1e-12, C_p within
+    1e-9."""
     if path == "v1":
         monkeypatch.setenv("TK_KERNELS", "v1")
+    if path == "tiled":
+        monkeypatch.setenv("TK_HAM_TILED", "1")
     n = O.space_size(radix)
     fit, ok = O.gen_iid(n, q, 31)
     ref = O.analyze(radix, fit, ok, O.HAMMING, nthreads=8, node_limit=1 << 32)
@@ -318,6 +326,9 @@ def test_hamming_tiled_pagerank_matches_oracle(tk, monkeypatch, path, radix, q):
         r = land.pagerank_vector()
         f_opt, _ = land.optimum()
         cps = land.centrality(f_opt, [k / 100.0 for k in range(16)])
+        used = land.kernel_info()["pagerank_kernel"]
+    if path == "staged" and n > 512:
+        assert used == "ham_staged", used
     assert it == ref["iterations"]
     assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
     assert abs(s - 1.0) < 1e-9
