@@ -68,6 +68,9 @@ VARIANTS = {
     "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
     "xnocomp0": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1", "-DTK_X_NODIM0=1"],
     "xhalf": ["-DTK_X_ITERS=29", "-DTK_X_HALFLDS=1"],
+    # staged Hamming timing experiments (wrong results)
+    "hxnw": ["-DTK_X_ITERS=37", "-DTK_HX_NOWAIT=1"],  # consumers do not wait for the ring data
+    "hxnc": ["-DTK_X_ITERS=37", "-DTK_HX_NOCOPY=1"],  # producers arrive without copying
 }
 
 

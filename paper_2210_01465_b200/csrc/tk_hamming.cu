@@ -239,57 +239,69 @@ __global__ void __launch_bounds__(kHT, TK_HAM_MINB)
 //
 // The tiled kernel above gathers every line value with a warp load and keeps
 // only two loads in flight per thread: it is bound by memory-level parallelism
-// (DRAM at ~20 %) and, sweeping in rank order, re-reads the lines of the
-// slowest dimensions from DRAM (~190 B per rank and iteration on C5).
+// (DRAM at ~20 %) and re-reads the lines of the slowest dimensions from DRAM
+// (~190 B per rank and iteration on C5).
 //
 // This kernel streams the lines through shared memory instead.  The dims split
 // into OUTER dims 0..k-1, whose strides are multiples of the tile (their digit
 // is fixed over a tile), and INNER dims k..D-1, whose lines stay inside the
 // aligned block of B = s_{k-1} ranks that holds the tile.  For a tile at v0:
 //   - every outer neighbour line (i, j) is one whole range c[v0 + (j - x_i) s_i,
-//     + T): producer warps copy the ranges with 1-D bulk copies (TMA) into a
-//     ring of T-double slots, one mbarrier pair per slot, in exactly the order
-//     the in-edge sum consumes them;
+//     + T).  A tile's R = sum_{i<k} (m_i - 1) ranges, in the order the in-edge
+//     sum consumes them, are cut into chunks of at most C ranges; a chunk is
+//     one ring stage with one full / empty mbarrier pair, filled by one
+//     producer warp with one 1-D bulk copy (TMA) per lane;
 //   - the inner lines come from a copy of the block (double-buffered).
+// Per-range barriers cost ~650 cycles per range in handshakes (measured: a
+// variant without any copies ran as slow), so the handshake is per chunk.
 // The in-edge sum keeps the oracle's order (ascending source rank): lower
 // ranges dims 0..k-1, inner lower / upper from the block, upper ranges dims
 // k-1..0 -- so r' stays bit-identical.
-//
-// Tiles are swept with the block offset fastest, then x_0, x_1, ... x_{k-1}:
-// the concurrently processed tiles of the grid share their outer lines, so
-// each line is read from DRAM once per sweep and re-read from L2 by its
-// siblings (the rank-order sweep of the tiled kernel misses L2 on dims 0-1).
 constexpr int kHsT = 512;                      // ranks per tile = consumer threads
 constexpr int kHsConsumerWarps = kHsT / 32;
-constexpr int kHsProdWarps = 4;
+constexpr int kHsProdWarps = 2;
 constexpr int kHsThreads = kHsT + 32 * kHsProdWarps;
-constexpr int kHsMaxSlots = 48;
+constexpr int kHsMaxStages = 8;
+constexpr int kHsMaxChunk = 16;                // ranges per stage (one lane each)
 constexpr int kHsMaxNear = 4096;               // block values (32 KB per buffer)
 
 struct HamStagePlan {
     int k;                                  // outer dims
     uint32_t B;                             // block = s_{k-1} ranks
     uint32_t tpb;                           // tiles per block = B / T
-    int slots;                              // ring slots
+    int R;                                  // outer ranges per tile
+    int C;                                  // ranges per stage (chunk)
+    int stages;                             // ring stages
+    int order;                              // tile sweep order (ham_tile_of)
     unsigned long long tpb_magic;           // fdiv by tpb (0 when tpb == 1)
     unsigned long long rmagic[kMaxDims];    // fdiv by radix[i]
 };
 
 struct HamPipe {
-    uint64_t full[kHsMaxSlots];
-    uint64_t empty[kHsMaxSlots];
+    uint64_t full[kHsMaxStages];
+    uint64_t empty[kHsMaxStages];
     uint64_t nfull[2];
     uint64_t nempty[2];
 };
 
-// sweep position g -> tile origin v0 and the outer digits (block offset
-// fastest, then x_0 .. x_{k-1})
+// sweep position g -> tile origin v0 and the outer digits.  hp.order 0: rank
+// order (tile g); 1: block offset fastest, then x_0 .. x_{k-1}
 template <int DIMS>
 __device__ __forceinline__ uint32_t ham_tile_of(const DevShape& s, const HamStagePlan& hp,
                                                 uint32_t g, uint32_t (&x)[DIMS],
                                                 uint32_t& w) {
     const uint32_t r0 = fdiv(g, hp.tpb_magic);
     w = g - r0 * hp.tpb;
+    if (hp.order == 0) {
+        const uint32_t v0 = g * kHsT;
+#pragma unroll
+        for (int i = 0; i < DIMS; ++i)
+            if (i < hp.k) {
+                const uint32_t q = fdiv(v0, s.magic[i]);
+                x[i] = q - fdiv(q, hp.rmagic[i]) * s.radix[i];
+            }
+        return v0;
+    }
     uint32_t r = r0, v0 = w * kHsT;
 #pragma unroll
     for (int i = 0; i < DIMS; ++i) {
@@ -301,6 +313,38 @@ __device__ __forceinline__ uint32_t ham_tile_of(const DevShape& s, const HamStag
         }
     }
     return v0;
+}
+
+// range r of a tile's consumption sequence -> signed line offset (j - x_i) s_i
+template <int DIMS>
+__device__ __forceinline__ long long ham_range_offset(const DevShape& s, const HamStagePlan& hp,
+                                                      const uint32_t (&x)[DIMS], int r) {
+    long long off = 0;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < DIMS; ++i)
+        if (i < hp.k && !found) {
+            if (r < static_cast<int>(x[i])) {
+                off = static_cast<long long>(r - static_cast<int>(x[i])) * s.stride[i];
+                found = true;
+            } else {
+                r -= static_cast<int>(x[i]);
+            }
+        }
+#pragma unroll
+    for (int ii = 0; ii < DIMS; ++ii) {
+        const int i = DIMS - 1 - ii;
+        if (i < hp.k && !found) {
+            const int up = static_cast<int>(s.radix[i] - 1 - x[i]);
+            if (r < up) {
+                off = static_cast<long long>(r + 1) * s.stride[i];
+                found = true;
+            } else {
+                r -= up;
+            }
+        }
+    }
+    return off;
 }
 
 template <int DIMS, typename MW>
@@ -315,13 +359,15 @@ __global__ void __launch_bounds__(kHsThreads, 1)
     const int t = threadIdx.x;
     const uint32_t G = gridDim.x;
     const uint32_t ntiles = a.n / kHsT;  // outer dims exist: T divides N
-    const int R = hp.slots;
+    const int S = hp.stages, C = hp.C;
+    const int nchunks = (hp.R + C - 1) / C;  // stages per tile
     const MW* __restrict__ inm = static_cast<const MW*>(a.inm);
     double* ring = reinterpret_cast<double*>(smem);
-    double* nearb = ring + static_cast<size_t>(R) * kHsT;
+    const size_t stage_elems = static_cast<size_t>(C) * kHsT;
+    double* nearb = ring + static_cast<size_t>(S) * stage_elems;
     if (t <= kMaxHamDeg) s_rcp[t] = t ? __drcp_rn(t) : 0.0;
     if (t == 0) {
-        for (int i = 0; i < R; ++i) {
+        for (int i = 0; i < S; ++i) {
             mbar_init(&pp.full[i], 1);
             mbar_init(&pp.empty[i], kHsConsumerWarps);
         }
@@ -355,15 +401,15 @@ __global__ void __launch_bounds__(kHsThreads, 1)
         D = block_sum<kHsThreads>(acc, s_red);
     }
 
-    // ring / block pipeline position (continues across sweeps on both sides)
-    int slot = 0;
-    uint32_t sph = 0;       // phase of the current ring slot
-    uint32_t uses = 0;      // ring uses so far (producer: skip the first-round waits)
-    uint32_t ntile = 0;     // tiles so far (block buffer = ntile & 1, phase = (ntile >> 1) & 1)
+    // ring position (continues across sweeps on both sides)
+    int st = 0;
+    uint32_t sph = 0;     // phase of stage st
+    uint32_t uses = 0;    // stage uses so far
+    uint32_t ntile = 0;   // tiles so far (block buffer ntile & 1, phase (ntile >> 1) & 1)
     auto advance = [&]() {
         ++uses;
-        if (++slot == R) {
-            slot = 0;
+        if (++st == S) {
+            st = 0;
             sph ^= 1u;
         }
     };
@@ -371,38 +417,64 @@ __global__ void __launch_bounds__(kHsThreads, 1)
     auto sweep = [&](const double* cc, double dn, double* out, bool final_pass, double& lres,
                      double& ldang, double& lsum) {
         if (t >= kHsT) {  // ------------------------------------------ producers
-            const int pw = (t - kHsT) >> 5;
-            const bool leader = (t & 31) == 0;
+            const int pw = (t - kHsT) >> 5, lane = t & 31;
             for (uint32_t g = blockIdx.x; g < ntiles; g += G, ++ntile) {
                 uint32_t x[DIMS], w;
                 const uint32_t v0 = ham_tile_of<DIMS>(s, hp, g, x, w);
-                if (pw == 0 && leader) {
+                if (pw == 0 && lane == 0) {
                     const int nb = ntile & 1;
                     if (ntile >= 2) mbar_wait(&pp.nempty[nb], ((ntile >> 1) & 1u) ^ 1u);
                     mbar_expect_tx(&pp.nfull[nb], hp.B * 8);
                     bulk_g2s(nearb + static_cast<size_t>(nb) * hp.B, cc + (v0 - w * kHsT),
                              hp.B * 8, &pp.nfull[nb]);
                 }
-                // ranges in consumption order; range q of the stream goes to warp q % P
-                auto issue = [&](int i, uint32_t j) {
-                    if (static_cast<int>(uses % kHsProdWarps) == pw && leader) {
-                        if (uses >= static_cast<uint32_t>(R)) mbar_wait(&pp.empty[slot], sph ^ 1u);
-                        mbar_expect_tx(&pp.full[slot], kHsT * 8);
-                        const double* src = cc + (v0 + (j - x[i]) * s.stride[i]);
-                        bulk_g2s(ring + static_cast<size_t>(slot) * kHsT, src, kHsT * 8,
-                                 &pp.full[slot]);
+                // chunk q of the stream is filled by producer warp q % P, one
+                // range per lane
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    if (static_cast<int>(uses % kHsProdWarps) == pw) {
+                        const int r0 = ch * C;
+                        const int cnt = min(C, hp.R - r0);
+                        if (lane == 0) {
+                            if (uses >= static_cast<uint32_t>(S)) mbar_wait(&pp.empty[st], sph ^ 1u);
+#ifndef TK_HX_NOCOPY
+                            mbar_expect_tx(&pp.full[st], static_cast<uint32_t>(cnt) * kHsT * 8);
+#else
+                            mbar_arrive(&pp.full[st]);  // timing experiment: no data movement
+#endif
+                        }
+                        __syncwarp();
+#ifndef TK_HX_NOCOPY
+                        if (lane < cnt) {
+                            const long long off = ham_range_offset<DIMS>(s, hp, x, r0 + lane);
+                            bulk_g2s(ring + st * stage_elems + static_cast<size_t>(lane) * kHsT,
+                                     cc + (static_cast<long long>(v0) + off), kHsT * 8, &pp.full[st]);
+                        }
+#endif
                     }
                     advance();
-                };
-                for (int i = 0; i < hp.k; ++i)
-                    for (uint32_t j = 0; j < x[i]; ++j) issue(i, j);
-                for (int i = hp.k - 1; i >= 0; --i)
-                    for (uint32_t j = x[i] + 1; j < s.radix[i]; ++j) issue(i, j);
+                }
             }
             return;
         }
         // ------------------------------------------------------- consumers
         const int lane = t & 31;
+        // in-masks and out-degrees are streamed kAhead tiles ahead of use
+        // (their DRAM latency would otherwise stall every warp of the CTA at
+        // the start of each tile: the warps move in lockstep through the ring)
+        constexpr int kAhead = 2;
+        auto rank_of = [&](uint32_t gg) -> uint32_t {
+            uint32_t xx[DIMS], ww;
+            return ham_tile_of<DIMS>(s, hp, gg, xx, ww) + t;
+        };
+        unsigned long long mq[kAhead];
+        uint32_t dq[kAhead];
+#pragma unroll
+        for (int i = 0; i < kAhead; ++i) {
+            const uint32_t gg = blockIdx.x + i * G;
+            const uint32_t vv = gg < ntiles ? rank_of(gg) : 0u;
+            mq[i] = gg < ntiles ? static_cast<unsigned long long>(__ldcs(inm + vv)) : 0ull;
+            dq[i] = gg < ntiles ? __ldcs(a.odeg + vv) : 0u;
+        }
         for (uint32_t g = blockIdx.x; g < ntiles; g += G, ++ntile) {
             uint32_t x[DIMS], w;
             const uint32_t v0 = ham_tile_of<DIMS>(s, hp, g, x, w);
@@ -414,52 +486,122 @@ __global__ void __launch_bounds__(kHsThreads, 1)
                     const uint32_t q = fdiv(o, s.magic[i]);
                     x[i] = q - fdiv(q, hp.rmagic[i]) * s.radix[i];
                 }
-            const unsigned long long mask = static_cast<unsigned long long>(__ldcs(inm + v));
-            const uint32_t deg = __ldcs(a.odeg + v);
+            const unsigned long long mask = mq[0];
+            const uint32_t deg = dq[0];
+#pragma unroll
+            for (int i = 0; i + 1 < kAhead; ++i) {
+                mq[i] = mq[i + 1];
+                dq[i] = dq[i + 1];
+            }
+            {
+                const uint32_t gg = g + kAhead * G;
+                const uint32_t vv = gg < ntiles ? rank_of(gg) : 0u;
+                mq[kAhead - 1] = gg < ntiles ? static_cast<unsigned long long>(__ldcs(inm + vv)) : 0ull;
+                dq[kAhead - 1] = gg < ntiles ? __ldcs(a.odeg + vv) : 0u;
+            }
+            // the tile's outer in-bits in consumption order: lower segments
+            // dims 0..k-1 (bits base_i + [0, x_i)), then upper segments dims
+            // k-1..0 (bits base_i + [x_i, m_i - 1)); L = lower ranges
+            unsigned long long seq = 0;
+            int L = 0, pos = 0;
+#pragma unroll
+            for (int i = 0; i < DIMS; ++i)
+                if (i < hp.k) {
+                    const int n = static_cast<int>(x[i]);
+                    if (n) seq |= ((mask >> s.base[i]) & (~0ull >> (64 - n))) << pos;
+                    pos += n;
+                }
+            L = pos;
+#pragma unroll
+            for (int ii = 0; ii < DIMS; ++ii) {
+                const int i = DIMS - 1 - ii;
+                if (i < hp.k) {
+                    const int n = static_cast<int>(s.radix[i] - 1 - x[i]);
+                    if (n) seq |= ((mask >> (s.base[i] + x[i])) & (~0ull >> (64 - n))) << pos;
+                    pos += n;
+                }
+            }
             double acc = 0.0;
-            auto take = [&](int bit) {
-                mbar_wait(&pp.full[slot], sph);
-                const double val = ring[static_cast<size_t>(slot) * kHsT + t];
-                if ((mask >> bit) & 1ull) acc = __dadd_rn(acc, val);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&pp.empty[slot]);
-                advance();
+            int rin = C;  // position in the open stage (C: none open)
+            const double* stg = ring;
+            // ranges [rb, re) of the sequence, stage by stage
+            auto outer = [&](int rb, int re) {
+                int r = rb;
+                while (r < re) {
+                    if (rin == C) {
+                        mbar_wait(&pp.full[st], sph);
+                        stg = ring + st * stage_elems + t;
+                        rin = 0;
+                    }
+                    const int n = min(C - rin, re - r);
+                    const double* p0 = stg + static_cast<size_t>(rin) * kHsT;
+                    // this call's n in-bits as a 32-bit word: immediate bit tests
+                    const uint32_t sb = static_cast<uint32_t>(seq >> r) &
+                                        (n >= 32 ? ~0u : ((1u << n) - 1u));
+#pragma unroll
+                    for (int q = 0; q < kHsMaxChunk; ++q) {
+                        if (q < n) {
+                            const double val = p0[static_cast<size_t>(q) * kHsT];
+                            if (sb & (1u << q)) acc = __dadd_rn(acc, val);
+                        }
+                    }
+                    rin += n;
+                    r += n;
+                    if (rin == C) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&pp.empty[st]);
+                        advance();
+                    }
+                }
             };
-            // lower neighbours of the outer dims (dims ascending, values ascending)
-            for (int i = 0; i < hp.k; ++i)
-                for (uint32_t j = 0; j < x[i]; ++j) take(s.base[i] + static_cast<int>(j));
-            // inner dims from the block copy
+            outer(0, L);  // lower neighbours of the outer dims
+            // inner dims from the block copy: warp-uniform trip counts (m_i - 1),
+            // the lane's own digit only in the predicate
             const int nb = ntile & 1;
             mbar_wait(&pp.nfull[nb], (ntile >> 1) & 1u);
             const double* blk = nearb + static_cast<size_t>(nb) * hp.B + o;
 #pragma unroll
             for (int i = 0; i < DIMS; ++i) {
                 if (i < hp.k) continue;
-                const uint32_t st = s.stride[i], xi = x[i];
-                const double* row = blk - static_cast<int>(xi * st);
-                const unsigned long long mi = mask >> s.base[i];
-#pragma unroll kHamUnroll
-                for (uint32_t j = 0; j < xi; ++j)
-                    if ((mi >> j) & 1ull) acc = __dadd_rn(acc, row[j * st]);
+                const uint32_t sti = s.stride[i], xi = x[i], m1 = s.radix[i] - 1;
+                const double* row = blk - static_cast<int>(xi * sti);
+                const uint32_t mi = static_cast<uint32_t>(mask >> s.base[i]);
+                if (m1 <= 8) {  // the usual radices: bit tests with immediates
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (j < m1 && j < xi && (mi & (1u << j))) acc = __dadd_rn(acc, row[j * sti]);
+                } else {
+                    for (uint32_t j = 0; j < m1; ++j)
+                        if (j < xi && ((mask >> (s.base[i] + j)) & 1ull))
+                            acc = __dadd_rn(acc, row[j * sti]);
+                }
             }
             const double cold = final_pass ? 0.0 : blk[0];
 #pragma unroll
             for (int ii = 0; ii < DIMS; ++ii) {
                 const int i = DIMS - 1 - ii;
                 if (i < hp.k) continue;
-                const uint32_t st = s.stride[i], xi = x[i], m = s.radix[i];
-                const double* row = blk - static_cast<int>(xi * st);
-                const unsigned long long mi = mask >> (s.base[i] + xi);
-#pragma unroll kHamUnroll
-                for (uint32_t j = xi + 1; j < m; ++j)
-                    if ((mi >> (j - xi - 1)) & 1ull) acc = __dadd_rn(acc, row[j * st]);
+                const uint32_t sti = s.stride[i], xi = x[i], m = s.radix[i];
+                const double* row = blk - static_cast<int>(xi * sti);
+                const uint32_t mi = static_cast<uint32_t>(mask >> s.base[i]);  // value j > x_i: bit j - 1
+                if (m <= 9) {
+#pragma unroll
+                    for (uint32_t j = 1; j < 9; ++j)
+                        if (j < m && j > xi && (mi & (1u << (j - 1)))) acc = __dadd_rn(acc, row[j * sti]);
+                } else {
+                    for (uint32_t j = 1; j < m; ++j)
+                        if (j > xi && ((mask >> (s.base[i] + j - 1)) & 1ull))
+                            acc = __dadd_rn(acc, row[j * sti]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&pp.nempty[nb]);
-            // upper neighbours of the outer dims (dims descending, values ascending)
-            for (int i = hp.k - 1; i >= 0; --i)
-                for (uint32_t j = x[i] + 1; j < s.radix[i]; ++j)
-                    take(s.base[i] + static_cast<int>(j) - 1);
+            outer(L, hp.R);  // upper neighbours of the outer dims
+            if (rin != C) {  // the tile's last, partial stage
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pp.empty[st]);
+                advance();
+            }
             const double xr = __dadd_rn(a.teleport, __dmul_rn(a.damping, __dadd_rn(acc, dn)));
             if (final_pass) {
                 out[v] = xr;
@@ -511,7 +653,11 @@ __global__ void __launch_bounds__(kHsThreads, 1)
         dn_last = dn;
         ++it;
         cur ^= 1;
+#ifdef TK_X_ITERS
+        if (it >= TK_X_ITERS) {
+#else
         if (res < a.tol) {
+#endif
             status = 0;
             break;
         }
@@ -567,7 +713,9 @@ void* ham_kernel(int dims) {
 // dim, and slots <= 64 (u64 in-mask).
 bool ham_staged_plan(const DevShape& s, int smem_budget, HamStagePlanOut* out) {
     if (s.kind != TK_HAMMING || s.dims < 2 || s.dims > 16 || s.slots > kMaxHamDeg) return false;
-    if (std::getenv("TK_HAM_TILED")) return false;  // A/B: keep the tiled kernel
+    // opt-in (TK_HAM_STAGED=1): correct, but slower than the tiled kernel on C5
+    // (454-468 vs 427-449 ms; profiles/r01_ab_log.md, round 2)
+    if (!std::getenv("TK_HAM_STAGED")) return false;
     int k = 0;
     while (k < s.dims && s.stride[k] >= static_cast<uint32_t>(kHsT)) ++k;
     if (k == 0 || k == s.dims) return false;
@@ -575,13 +723,27 @@ bool ham_staged_plan(const DevShape& s, int smem_budget, HamStagePlanOut* out) {
         if (s.stride[i] % kHsT) return false;
     const uint32_t B = s.stride[k - 1];
     if (B > static_cast<uint32_t>(kHsMaxNear)) return false;
+    int R = 0;
+    for (int i = 0; i < k; ++i) R += static_cast<int>(s.radix[i]) - 1;
     const long long ring_bytes = smem_budget - 2ll * B * 8 - 256;
-    int slots = static_cast<int>(ring_bytes / (kHsT * 8));
-    if (slots > kHsMaxSlots) slots = kHsMaxSlots;
-    if (slots < 4) return false;
+    // chunk: the fewest stages per tile that still leave >= 3 stages in the ring
+    int C = 0, S = 0;
+    for (int per = 1; per <= R; ++per) {
+        const int c = (R + per - 1) / per;
+        if (c > kHsMaxChunk) continue;
+        const int st = static_cast<int>(ring_bytes / (static_cast<long long>(c) * kHsT * 8));
+        if (st >= 3) {
+            C = c;
+            S = st > kHsMaxStages ? kHsMaxStages : st;
+            break;
+        }
+    }
+    if (!C) return false;
     out->k = k;
     out->B = B;
-    out->slots = slots;
+    out->R = R;
+    out->C = C;
+    out->stages = S;
     return true;
 }
 
@@ -592,12 +754,18 @@ cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamSt
     hp.k = po.k;
     hp.B = po.B;
     hp.tpb = po.B / kHsT;
-    hp.slots = po.slots;
+    hp.R = po.R;
+    hp.C = po.C;
+    hp.stages = po.stages;
     hp.tpb_magic = magic_of(hp.tpb);
+    {
+        const char* e = std::getenv("TK_HAM_ORDER");  // A/B: 0 rank order, 1 digit order
+        hp.order = e ? std::atoi(e) : 0;
+    }
     for (int i = 0; i < s.dims; ++i) hp.rmagic[i] = magic_of(s.radix[i]);
     void* k = wide ? ham_staged_kernel<unsigned long long>(s.dims) : ham_staged_kernel<uint32_t>(s.dims);
     if (!k) return cudaErrorInvalidValue;
-    const int smem = po.slots * kHsT * 8 + 2 * static_cast<int>(po.B) * 8;
+    const int smem = po.stages * po.C * kHsT * 8 + 2 * static_cast<int>(po.B) * 8;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int bps = 0;
@@ -609,8 +777,8 @@ cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamSt
     if (g > ntiles) g = ntiles;
     *grid_out = static_cast<int>(g);
     if (std::getenv("TK_DEBUG"))
-        std::fprintf(stderr, "[tk] pagerank_ham_staged k=%d B=%u slots=%d grid=%llu smem=%d\n",
-                     hp.k, hp.B, hp.slots, static_cast<unsigned long long>(g), smem);
+        std::fprintf(stderr, "[tk] pagerank_ham_staged k=%d B=%u R=%d C=%d stages=%d grid=%llu smem=%d\n",
+                     hp.k, hp.B, hp.R, hp.C, hp.stages, static_cast<unsigned long long>(g), smem);
     DevShape sc = s;
     PrArgs ac = a;
     void* args[] = {&sc, &hp, &ac};

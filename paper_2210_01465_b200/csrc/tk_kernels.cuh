@@ -150,7 +150,9 @@ bool ham_tiled_supported(const DevShape& s);
 struct HamStagePlanOut {
     int k;        // outer dims
     uint32_t B;   // block ranks (s_{k-1})
-    int slots;    // ring slots of 512 doubles
+    int R;        // outer ranges per tile
+    int C;        // ranges per ring stage
+    int stages;   // ring stages
 };
 bool ham_staged_plan(const DevShape& s, int smem_budget, HamStagePlanOut* out);
 cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamStagePlanOut& p,

@@ -314,8 +314,8 @@ def test_hamming_tiled_pagerank_matches_oracle(tk, monkeypatch, path, radix, q):
     1e-9."""
     if path == "v1":
         monkeypatch.setenv("TK_KERNELS", "v1")
-    if path == "tiled":
-        monkeypatch.setenv("TK_HAM_TILED", "1")
+    if path == "staged":
+        monkeypatch.setenv("TK_HAM_STAGED", "1")
     n = O.space_size(radix)
     fit, ok = O.gen_iid(n, q, 31)
     ref = O.analyze(radix, fit, ok, O.HAMMING, nthreads=8, node_limit=1 << 32)
