@@ -510,3 +510,43 @@ def test_c5_full_size_parity(tk):
     assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
     for k, c in ref["c_p_curve"]:
         assert abs(s.c_p[k] - c) <= CP_ATOL
+
+
+def test_c4_bench_workload_matches_oracle(tk):
+    """The C4 bench workload itself (bench.c4_landscapes: 4 paper shapes + 22
+    seeded shapes x 9 seeds, 234 landscapes) through tk.BatchAnalyzer, against
+    the oracle: iterations, edge and minima counts exact, C_p curve within 1e-9,
+    report rows (minima ranks and fitness bit-exact, fraction of optimum exact,
+    PageRank of each minimum within 1e-12 of the oracle's)."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    tables = []
+    for _name, radix, q, seed in bench.c4_landscapes():
+        fit, ok = O.gen_synthetic(list(radix), q, "rugged", seed)
+        tables.append((list(radix), np.ascontiguousarray(fit, np.float64),
+                       np.ascontiguousarray(ok, np.uint8)))
+    refs = [O.analyze(radix, fit, ok, O.ADJACENT, node_limit=1 << 32) for radix, fit, ok in tables]
+    bufs = [[np.empty(max(1, len(r["ffg"]["minima"])), dt)
+             for dt in (np.uint64, np.float64, np.float64, np.float64)] for r in refs]
+    items = [(radix, f.ctypes.data, o.ctypes.data) for radix, f, o in tables]
+    with tk.BatchAnalyzer(workers=8) as batch:
+        got = batch.run(items, tk.ADJACENT, [tuple(b.ctypes.data for b in bb) for bb in bufs],
+                        node_limit=1 << 32)
+    assert len(got) == 234
+    for (radix, fit, ok), s, ref, bb in zip(tables, got, refs, bufs):
+        g = ref["ffg"]
+        mins = g["minima"]
+        assert s.iterations == ref["iterations"], radix
+        assert s.n_edges == len(g["targets"]) and s.n_minima == len(mins)
+        for k, c in ref["c_p_curve"]:
+            assert abs(s.c_p[k] - c) <= CP_ATOL
+        ranks, fmin, frac, prm = (b[: len(mins)] for b in bb)
+        f_opt = fit[ok.astype(bool)].min()
+        assert np.array_equal(ranks, mins.astype(np.uint64))
+        assert np.array_equal(fmin.view(np.uint64), fit[mins].view(np.uint64))
+        assert np.array_equal(frac, f_opt / fit[mins])
+        assert np.max(np.abs(prm - ref["pagerank"][mins]), initial=0.0) <= 1e-12
