@@ -16,8 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtk_landscape.so")
-SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_descent.cu",
-           "tk_abi.cu"]
+SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_ring.cu",
+           "tk_descent.cu", "tk_abi.cu"]
 HEADERS = ["tk_internal.cuh", "tk_kernels.cuh", "tk_pipe.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -68,6 +68,12 @@ VARIANTS = {
     "xnocomp": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1"],
     "xnocomp0": ["-DTK_X_ITERS=29", "-DTK_X_NOCOMP=1", "-DTK_X_NODIM0=1"],
     "xhalf": ["-DTK_X_ITERS=29", "-DTK_X_HALFLDS=1"],
+    "spw": ["-DTK_STAGE_PW=1"],  # packed words staged by the producers
+    "xnopw": ["-DTK_X_ITERS=29", "-DTK_X_NOPW=1"],  # no packed-word loads
+    "xnofillnopw": ["-DTK_X_ITERS=29", "-DTK_X_NOPW=1", "-DTK_X_NOFILL=1"],
+    "xnodadd": ["-DTK_X_ITERS=29", "-DTK_X_NODADD=1"],  # loads kept, fp64 chain replaced by XOR
+    "xnofill": ["-DTK_X_ITERS=29", "-DTK_X_NOFILL=1"],  # no bulk copies into the stages
+    "xnofilldadd": ["-DTK_X_ITERS=29", "-DTK_X_NOFILL=1", "-DTK_X_NODADD=1"],
     # staged Hamming timing experiments (wrong results)
     "hxnw": ["-DTK_X_ITERS=37", "-DTK_HX_NOWAIT=1"],  # consumers do not wait for the ring data
     "hxnc": ["-DTK_X_ITERS=37", "-DTK_HX_NOCOPY=1"],  # producers arrive without copying

@@ -430,7 +430,7 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                  double d, double tol, int64_t max_iter, cudaEvent_t e0 = nullptr,
                  cudaEvent_t e1 = nullptr, float* ms = nullptr, int* grid = nullptr,
                  const tk::StagePlan* plan = nullptr, const tk::RowPlan* rplan = nullptr,
-                 int smem_budget = 0, int* kernel_used = nullptr) {
+                 int smem_budget = 0, int* kernel_used = nullptr, bool ring = false) {
     const int maxg = (plan || rplan) ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
     TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
@@ -460,7 +460,8 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                             smem_budget > 0 && tk::ham_staged_plan(s, smem_budget, &hplan);
     const bool ham_tiled = !plan && !ham_staged && mode == tk::MODE_HAM && staged_enabled() &&
                            tk::ham_tiled_supported(s);
-    TKC(gated_coop_launch(device, num_sms, (ham_tiled || ham_staged) ? num_sms : footprint, stream, [&] {
+    TKC(gated_coop_launch(device, num_sms, (ham_tiled || ham_staged || ring) ? num_sms : footprint, stream, [&] {
+        if (ring) return tk::launch_pagerank_ring(s, a, smem_budget, num_sms, &g, stream);
         if (rplan) return tk::launch_pagerank_rows(s, *rplan, a, num_sms, &g, stream);
         if (plan) return tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream);
         if (ham_staged)
@@ -469,8 +470,9 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
         return tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
     }));
     if (e1) TKC(cudaEventRecord(e1, stream));
-    // 0 per-lane, 1 staged (Adjacent), 2 row-tiled, 3 Hamming staged, 4 Hamming tiled
-    if (kernel_used) *kernel_used = rplan ? 2 : plan ? 1 : ham_staged ? 3 : ham_tiled ? 4 : 0;
+    // 0 per-lane, 1 staged (Adjacent), 2 row-tiled, 3 Hamming staged, 4 Hamming tiled, 5 ring
+    if (kernel_used)
+        *kernel_used = ring ? 5 : rplan ? 2 : plan ? 1 : ham_staged ? 3 : ham_tiled ? 4 : 0;
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
     TKC(cudaStreamSynchronize(stream));
     if (e0 && e1 && ms) TKC(cudaEventElapsedTime(ms, e0, e1));
@@ -501,14 +503,17 @@ int do_pagerank(tk_land* l, double d, double tol, int64_t max_iter) {
     tk::RowPlan rplan{};
     const bool have_rows = l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
                            tk::make_row_plan(l->shape, l->num_sms, &rplan);
-    const bool have_plan = !have_rows && l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+    const bool have_ring = !have_rows && l->mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+                           tk::ring_plan_available(l->shape, stage_budget(l), l->num_sms);
+    const bool have_plan = !have_rows && !have_ring && l->mode == tk::MODE_ADJ_PACKED &&
+                           staged_enabled() &&
                            tk::make_stage_plan(l->shape, true, stage_budget(l), &plan, false);
     l->pr_staged = have_rows ? 2 : have_plan ? 1 : 0;
     l->pr_done = false;
     st = run_pagerank(l->device, l->num_sms, l->shape, l->mode, l->wide, a, l->part,
                       l->small.as<Small>(), l->hsmall, l->stream, d, tol, max_iter, l->ev[2],
                       l->ev[3], &l->ms_pr, &l->pr_grid, have_plan ? &plan : nullptr,
-                      have_rows ? &rplan : nullptr, stage_budget(l), &l->pr_staged);
+                      have_rows ? &rplan : nullptr, stage_budget(l), &l->pr_staged, have_ring);
     if (st) return st;
     const PrOut& o = l->hsmall->pr;
     l->iterations = o.iter;

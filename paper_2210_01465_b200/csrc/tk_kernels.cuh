@@ -145,6 +145,11 @@ int pagerank_max_grid(int mode, bool wide, int num_sms);
 // Hamming: tiled contribution-only kernel (tk_hamming.cu) for shapes whose
 // digits align with 512-rank tiles; cudaErrorNotSupported otherwise
 bool ham_tiled_supported(const DevShape& s);
+// Adjacent: ring kernel (tk_ring.cu) -- per-CTA shared-memory ring of c over
+// chunks of consecutive tiles; far ranges staged per tile
+bool ring_plan_available(const DevShape& s, int smem_budget, int num_sms);
+cudaError_t launch_pagerank_ring(const DevShape& s, const PrArgs& a, int smem_budget, int num_sms,
+                                 int* grid_out, cudaStream_t stream);
 // Hamming: staged kernel (tk_hamming.cu) -- outer lines streamed through a
 // shared-memory ring with TMA bulk copies, inner lines from a block copy
 struct HamStagePlanOut {

@@ -277,6 +277,8 @@ def test_staged_and_v1_paths_match_oracle(tk, monkeypatch, path, radix, q):
 ])
 def test_row_tiled_pagerank_matches_oracle(tk, monkeypatch, rows, radix, q):
     monkeypatch.setenv("TK_PR_ROWS", "0" if rows == "staged" else "1")
+    if rows == "staged":
+        monkeypatch.setenv("TK_PR_STAGED", "1")
     if rows == "rows_win":  # the largest window the ring allows, however few columns
         monkeypatch.setenv("TK_ROW_MINCOLS", "1")
     n = O.space_size(radix)
@@ -550,3 +552,36 @@ def test_c4_bench_workload_matches_oracle(tk):
         assert np.array_equal(fmin.view(np.uint64), fit[mins].view(np.uint64))
         assert np.array_equal(frac, f_opt / fit[mins])
         assert np.max(np.abs(prm - ref["pagerank"][mins]), initial=0.0) <= 1e-12
+
+
+# Ring PageRank (tk_ring.cu): chunks of consecutive tiles per CTA, a shared-
+# memory ring of c for the dims within the ring's reach, far ranges staged.
+# Small chunks (TK_RING_CHUNK) make the kernel eligible at test sizes and put
+# many chunk boundaries (drain + warm-up) into every sweep.
+@pytest.mark.parametrize("chunk", ["2", "3", "4", "16"])
+@pytest.mark.parametrize("radix,q", [
+    ([8, 8, 6, 6, 4, 4, 4, 2, 2], 0.1),    # C5's lower dims: ring dims 2.., far dims 0-1
+    ([16, 12, 8, 8, 8, 4, 2, 2], 0.3),     # C2 shape
+    ([6, 10, 8, 6, 4, 4, 4, 2], 0.2),      # ring reach not a power of two
+    ([3, 5, 7, 9, 16, 16, 2], 0.15),       # odd radices, far stride 4608 (even)
+    ([40, 32, 24, 16], 0.05),              # 4 dims
+    ([7, 3, 5, 6, 4, 4, 4, 2, 2, 3], 0.1), # N = 1935360, odd tile count
+])
+def test_ring_pagerank_matches_oracle(tk, monkeypatch, chunk, radix, q):
+    monkeypatch.setenv("TK_RING_CHUNK", chunk)
+    monkeypatch.setenv("TK_PR_RING", "1")
+    n = O.space_size(radix)
+    if (n + 511) // 512 < 148 * int(chunk):
+        pytest.skip("fewer tiles than one chunk per SM")
+    fit, ok = O.gen_iid(n, q, 41)
+    ref = O.analyze(radix, fit, ok, O.ADJACENT, nthreads=8, node_limit=1 << 32)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        s = land.analyze(tk.ADJACENT, node_limit=1 << 32)
+        r = land.pagerank_vector()
+        info = land.kernel_info()
+    assert info["pagerank_kernel"] == "ring", info
+    assert s.iterations == ref["iterations"]
+    assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
+    for k, c in ref["c_p_curve"]:
+        assert abs(s.c_p[k] - c) <= CP_ATOL
