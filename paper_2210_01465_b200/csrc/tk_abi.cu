@@ -267,7 +267,34 @@ int do_build(tk_land* l, int kind, uint64_t node_limit, int emit) {
     a.ntiles = ntiles;
     TKC(cudaEventRecord(l->ev[0], l->stream));
     tk::StagePlan plan{};
-    if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+    // one-pass build (count + warp-slot look-back + CSR emission), opt-in with
+    // TK_FFG_FUSED=1: correct, but the look-back over the warp slots of the
+    // tiles in flight (~2,400 slots) serialises it: 15 ms vs 3.4 ms for the
+    // count / scan / fill kernels on C5 (profiles/r01_ab_log.md, round 2)
+    const bool fused = emit && !l->sharded && mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
+                       std::getenv("TK_FFG_FUSED") &&
+                       tk::make_stage_plan(s, false,
+                                           stage_budget(l) - static_cast<int>(tk::fused_seg_bytes()),
+                                           &plan);
+    if (fused) {
+        plan.fast = l->fit_clean && !std::getenv("TK_FFG_SLOW") ? 1 : 0;
+        const uint32_t nt = static_cast<uint32_t>((n + plan.T - 1) / plan.T);
+        a.ntiles = nt;
+        a.tile_lo = 0;
+        const size_t ns = static_cast<size_t>(nt) * (plan.T / 32);
+        TKC(ensure(l->tile_base, (ns + 1) * 16));
+        a.e_status = l->tile_base.as<unsigned long long>();
+        a.m_status = a.e_status + (ns + 1);
+        TKC(ensure(l->opt_part, static_cast<size_t>(l->num_sms) * 4 * 16));
+        a.opt_part_f = l->opt_part.as<double>();
+        a.opt_part_r = reinterpret_cast<unsigned long long*>(a.opt_part_f + l->num_sms * 4);
+        a.f_opt = &ds->f_opt;
+        a.opt_rank = &ds->rank;
+        a.opt_has = &ds->has;
+        l->opt_ready = true;
+        TKC(tk::launch_ffg_build_fused(s, plan, a, l->num_sms, l->stream));
+        l->staged = true;
+    } else if (mode == tk::MODE_ADJ_PACKED && staged_enabled() &&
         tk::make_stage_plan(s, false, stage_budget(l), &plan)) {
         plan.fast = l->fit_clean && !std::getenv("TK_FFG_SLOW") ? 1 : 0;
         // T-rank tiles over the whole space, or over this handle's shard

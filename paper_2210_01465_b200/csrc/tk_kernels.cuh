@@ -208,6 +208,9 @@ bool make_stage_plan(const DevShape& s, bool kind_pr, int smem_budget, StagePlan
                      bool stage_r = true);
 // count (staged) -> tile scans -> fill; a.e_status/m_status/tile_counter are the
 // scan scratch (>= ceil(ntiles/256) tiles), totals[0..1] are written by the scan.
+size_t fused_seg_bytes();
+cudaError_t launch_ffg_build_fused(const DevShape& s, const StagePlan& p, const BuildArgs& a,
+                                   int num_sms, cudaStream_t stream);
 cudaError_t launch_ffg_build_staged(const DevShape& s, const StagePlan& p, bool emit,
                                     const BuildArgs& a, int num_sms, cudaStream_t stream);
 cudaError_t launch_pagerank_staged(const DevShape& s, const StagePlan& p, const PrArgs& a,

@@ -585,3 +585,22 @@ def test_ring_pagerank_matches_oracle(tk, monkeypatch, chunk, radix, q):
     assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
     for k, c in ref["c_p_curve"]:
         assert abs(s.c_p[k] - c) <= CP_ATOL
+
+
+@pytest.mark.parametrize("radix,q", [
+    ([8, 6, 3, 3, 2], 0.52),
+    ([16, 12, 8, 8, 8, 4, 2, 2], 0.3),     # C2 shape: 49,152 warp slots of look-back
+    ([7, 3, 5, 6, 4, 4, 4, 2, 2, 3], 0.1), # N not a multiple of the tile
+])
+def test_fused_ffg_build_matches_oracle(tk, monkeypatch, radix, q):
+    """The one-pass FFG build (TK_FFG_FUSED=1: count, warp-slot decoupled
+    look-back and CSR emission in one kernel) is bit-exact against the oracle."""
+    monkeypatch.setenv("TK_FFG_FUSED", "1")
+    fit, ok = O.gen_synthetic(radix, q, "rugged", 4)
+    ref = O.build_ffg(radix, fit, ok, O.ADJACENT, node_limit=1 << 32, nthreads=8)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        land.build_ffg(O.ADJACENT, node_limit=1 << 32, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+    assert np.array_equal(off, ref["offsets"]) and np.array_equal(tg, ref["targets"])
+    assert np.array_equal(sk, ref["is_sink"]) and np.array_equal(mn, ref["minima"])
