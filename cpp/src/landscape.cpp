@@ -217,3 +217,24 @@ MinimaFractionReport minima_fraction_report(const SearchSpaceCache& cache, Neigh
 }
 
 }  // namespace tunekit
+
+namespace tunekit {
+
+// SURVEY.md s8(f) row 3 over tk_descents (include/tk_landscape.h)
+DescentReport random_descents(const SearchSpaceCache& cache, NeighbourhoodKind kind,
+                              std::uint64_t walkers, std::uint64_t seed, bool restart_scan) {
+    Land land = upload(cache);
+    std::uint64_t e = 0, m = 0;
+    check(tk_ffg_build(land.get(), kind_code(kind), std::numeric_limits<std::uint64_t>::max(), 0,
+                       &e, &m));
+    DescentReport rep;
+    std::vector<std::uint32_t> mins(m);
+    if (m) check(tk_ffg_copy_out(land.get(), nullptr, nullptr, nullptr, mins.data()));
+    rep.minima.assign(mins.begin(), mins.end());
+    rep.arrivals.resize(m);
+    check(tk_descents(land.get(), walkers, seed, restart_scan ? 1 : 0,
+                      m ? rep.arrivals.data() : nullptr, &rep.fail_arrivals, &rep.evaluations));
+    return rep;
+}
+
+}  // namespace tunekit

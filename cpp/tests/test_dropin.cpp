@@ -75,6 +75,13 @@ int main(int argc, char** argv) {
         std::ofstream fr(dir + "/fraction_" + k + ".txt");
         fr << std::hexfloat << mf.median << ' ' << mf.mean << ' ' << mf.fractions.size() << '\n';
         dump(dir + "/fraction_" + k + ".bin", mf.fractions);
+        const DescentReport dr = random_descents(cache, kind, 100000, 7);
+        dump(dir + "/descents_" + k + "_arrivals.bin", dr.arrivals);
+        {
+            std::ofstream df(dir + "/descents_" + k + ".txt");
+            df << dr.fail_arrivals << ' ' << dr.evaluations << '\n';
+        }
+        EXPECT(dr.minima.size() == g.minima.size());
         EXPECT(rep.minima.size() == g.minima.size());
         EXPECT(mf.fractions.size() == g.minima.size());
         if (kind == NeighbourhoodKind::Adjacent) {

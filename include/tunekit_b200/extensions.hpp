@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "tunekit/landscape.hpp"
 
@@ -24,5 +25,22 @@ CentralityReport analyze_landscape_limited(const SearchSpaceCache& cache, Neighb
 CentralityReport analyze_cache_file(const std::string& path, NeighbourhoodKind kind,
                                     double damping, int p_max_percent, std::uint64_t node_limit,
                                     ParameterSpace* space_out = nullptr);
+
+// The GPU random-walk validator: `walkers` randomized
+// first-improvement descents -- hillclimb.cpp:48-87 climb_random_first, with a
+// fresh scan order after every move when restart_scan -- from uniform starts,
+// all on the device (tk_descents).  Walker w draws from its own splitmix64
+// stream (seed, w), so the result is deterministic.  arrivals[i] counts the
+// descents that ended at minima[i] (the FFG minima, ascending); fail_arrivals
+// those that ended on a failed sink.  SPEC.md:430: the arrival frequencies
+// track PageRank over the minima.
+struct DescentReport {
+    std::vector<std::uint64_t> minima;
+    std::vector<std::uint64_t> arrivals;
+    std::uint64_t fail_arrivals = 0;
+    std::uint64_t evaluations = 0;
+};
+DescentReport random_descents(const SearchSpaceCache& cache, NeighbourhoodKind kind,
+                              std::uint64_t walkers, std::uint64_t seed, bool restart_scan = true);
 
 }  // namespace tunekit

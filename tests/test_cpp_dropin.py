@@ -55,7 +55,8 @@ def test_dropin_links_the_reference_host_classes(built):
     for sym in ("tunekit::build_ffg", "tunekit::pagerank", "tunekit::analyze_landscape",
                 "tunekit::proportion_of_centrality", "tunekit::classify_points",
                 "tunekit::minima_fraction_report", "tunekit::export_graph",
-                "tunekit::write_minima_csv", "tunekit::write_cp_curve_csv"):
+                "tunekit::write_minima_csv", "tunekit::write_cp_curve_csv",
+                "tunekit::random_descents"):
         assert sym in mine, sym
     for sym in ("tunekit::ParameterSpace::rank_of", "tunekit::SearchSpaceCache::finalize",
                 "tunekit::generate_synthetic_kernel_space", "tunekit::load_cache"):
@@ -194,6 +195,13 @@ def test_dropin_on_gpu_matches_oracle(built, tmp_path):
             acc += float(x)
         assert int(cnt) == k and float.fromhex(med) == want_med
         assert float.fromhex(mean) == acc / k
+        # random_descents (extensions.hpp): the device validator through C++,
+        # bit-identical to the oracle's restatement of climb_random_first
+        counts, ev = O.descents(radix, fit, kind, 100000, 7)
+        arr = rd(f"descents_{name}_arrivals.bin", np.uint64)
+        assert np.array_equal(arr, counts[g["minima"]].astype(np.uint64))
+        fa, dev = map(int, open(os.path.join(tmp_path, f"descents_{name}.txt")).read().split())
+        assert fa == 100000 - int(counts[g["minima"]].sum()) and dev == ev
         if kind == O.ADJACENT:
             _check_graph_exports(tmp_path, fit, ok, g)
 
