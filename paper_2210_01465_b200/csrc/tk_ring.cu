@@ -9,17 +9,23 @@
 // rank; the copies alone run in 24 ms, the consumers alone in 21 ms, together
 // 33 ms -- both sides share the SM's shared-memory datapath.
 //
-// Here each CTA sweeps CHUNKS of consecutive tiles and keeps a ring of the
-// last W tiles of c in shared memory.  Every dimension whose stride is at most
-// A tiles (C5: dims 4-11, strides <= 6144) reads its neighbours from the ring;
-// per tile the producers copy ONE new ring tile (the leading edge, tile k + A)
-// and the far ranges of the remaining dims (C5: dims 0-3, 8 ranges).  That is
-// 9 values per rank instead of 14 (plus a warm-up of 2A tiles per chunk).
-// The ring tile of rank v is v / T mod W; W >= 2A + S (S pipeline stages)
-// keeps every tile a consumer may still read out of the producer's way, and
-// at a chunk boundary the producer drains the pipeline before the warm-up.
-// Chunks are dealt round-robin to the CTAs, so the concurrently swept chunks
-// still share their far ranges in L2 (the front is G * chunk tiles wide).
+// Here each CTA sweeps CHUNKS of consecutive tiles and keeps the last W = 8
+// tiles of c in a shared-memory ring: tile k lives in slot k mod W, and the
+// first / last A slots are mirrored past the ends, so the window [k - A, k + A]
+// a consumer reads is linear and every neighbour source is one uniform pointer
+// per tile.  Dims with stride <= A tiles (C5, A = 2: dims 5-11) read the ring;
+// per tile the producers copy one new ring tile (plus its mirror for 2A of the W
+// slots) and the far ranges of the other dims (C5: dims 0-4, 10 ranges): 11.5
+// values per rank instead of 14.  W >= 2A + S (S stages) keeps every slot a
+// consumer may still read out of the producers' way; at a chunk boundary the
+// producer drains the pipeline before the warm-up.  Chunks are dealt
+// round-robin to the CTAs.
+//
+// Measured (C5, profiles/r01_ab_log.md round 2): 57-58 ms against 33 ms for the
+// staged kernel.  The consumers wait on the stage barriers (30 % of the stall
+// samples): the chunked sweep turns the grid's far-range reads from a few
+// contiguous fronts into ~1,500 scattered 4 KB streams (L2 hit 50 vs 61 %,
+// DRAM read 106 vs 89 GB per launch).  Opt-in: TK_PR_RING=1.
 #include <cooperative_groups.h>
 
 #include <cstdio>
@@ -38,8 +44,7 @@ constexpr int kRT = 512;                          // ranks per tile = consumer t
 constexpr int kRConsumerWarps = kRT / 32;
 constexpr int kRProdWarps = 4;
 constexpr int kRThreads = kRT + 32 * kRProdWarps;
-constexpr int kRW = 32;                           // ring tiles
-constexpr uint32_t kRMask = kRW * kRT - 1;        // ring element index mask
+constexpr int kRW = 8;                            // ring slots (tile k -> slot k mod W)
 constexpr int kRMaxStages = 4;
 constexpr int kRMaxFar = 2 * kMaxDims;
 constexpr int kRPwAhead = 2;
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
         mine += min(chunk, ntiles - c * chunk);
     const int S = p.stages;
     double* ring = reinterpret_cast<double*>(smem);
-    double* stages = ring + kRW * kRT;
+    double* stages = ring + static_cast<size_t>(kRW + 2 * p.A) * kRT;
     if (t <= kPackedSlots) s_rcp[t] = t ? __drcp_rn(t) : 0.0;
     if (t == 0) {
         for (int i = 0; i < S; ++i) {
@@ -146,12 +151,14 @@ __global__ void __launch_bounds__(kRThreads, 1)
                     const uint32_t pk = kk - 1;
                     mbar_wait(&pp.empty[pk % S], (pk / S) & 1u);
                 }
-                // copies of this tile: far ranges f < nfar, the ring's leading
-                // edge (tile k + A), and at a chunk start the ring warm-up
-                // (tiles k - A .. k + A - 1); copy q goes to lane q / P of warp q % P
-                const int nwarm = first ? 2 * p.A : 0;
-                const int ncopy = p.nfar + 1 + nwarm;
-                // copy q of this tile -> (src, dst, bytes); 0 bytes when empty
+                // copies of this tile: far ranges f < nfar into the stage, then
+                // ring tiles -- the leading edge k + A and, at a chunk start, the
+                // warm-up k - A .. k + A - 1 -- each into its slot's main position
+                // and, for the first / last A slots, its mirror position (so that
+                // every window [k - A, k + A] is linear in shared memory).
+                // Copy q goes to lane q / P of warp q % P.
+                const int nring = first ? 2 * p.A + 1 : 1;
+                const int ncopy = p.nfar + 2 * nring;
                 auto copy_of = [&](int q, const double*& src, double*& dst, bool& ef) -> uint32_t {
                     ef = false;
                     if (q < p.nfar) {
@@ -165,14 +172,21 @@ __global__ void __launch_bounds__(kRThreads, 1)
                         ef = (p.far_ef >> q) & 1u;
                         return static_cast<uint32_t>((bb - aa + 1) & ~1ll) * 8;
                     }
-                    const long long rt = q == p.nfar
-                                             ? static_cast<long long>(k) + p.A
-                                             : static_cast<long long>(k) - p.A + (q - p.nfar - 1);
+                    const int rq = q - p.nfar, ri = rq >> 1, mirror = rq & 1;
+                    const long long rt = ri == 0 ? static_cast<long long>(k) + p.A
+                                                 : static_cast<long long>(k) - p.A + (ri - 1);
                     if (rt < 0 || rt >= static_cast<long long>(ntiles)) return 0u;
+                    const int slot = static_cast<int>(rt % kRW);
+                    int pos = slot + p.A;
+                    if (mirror) {
+                        if (slot < p.A) pos = slot + p.A + kRW;
+                        else if (slot >= kRW - p.A) pos = slot + p.A - kRW;
+                        else return 0u;
+                    }
                     const long long v0 = rt * kRT;
                     const long long cnt = v0 + kRT > static_cast<long long>(a.n) ? a.n - v0 : kRT;
                     src = cc + v0;
-                    dst = ring + static_cast<size_t>(rt & (kRW - 1)) * kRT;
+                    dst = ring + static_cast<size_t>(pos) * kRT;
                     return static_cast<uint32_t>((cnt + 1) & ~1ll) * 8;
                 };
                 // copy q goes to lane q / P of warp q % P; each warp announces its
@@ -215,14 +229,6 @@ __global__ void __launch_bounds__(kRThreads, 1)
         uint32_t wq[kRPwAhead];
 #pragma unroll
         for (int i = 0; i < kRPwAhead; ++i) wq[i] = pw_of(i);
-        // ring direction j -> byte offset t + o_j (o_j = -+s_i) modulo the ring;
-        // per tile only the tile's ring origin is added
-        uint32_t roff[2 * DIMS];
-#pragma unroll
-        for (int i = 0; i < DIMS; ++i) {
-            roff[i] = (static_cast<uint32_t>(t) - s.stride[i]) * 8u;
-            roff[2 * DIMS - 1 - i] = (static_cast<uint32_t>(t) + s.stride[i]) * 8u;
-        }
         uint32_t k = blockIdx.x * chunk, inch = 0;  // current tile, position in its chunk
         // the prefetch tile (m + kRPwAhead), advanced the same way
         uint32_t kp = ring_tile(kRPwAhead, blockIdx.x, G, chunk), inchp = kRPwAhead % chunk;
@@ -244,28 +250,23 @@ __global__ void __launch_bounds__(kRThreads, 1)
             }
             mbar_wait(&pp.full[st], ph);
             const uint32_t mask = w & kRPackMask;
-            const uint32_t rbt = (k * kRT + t) & kRMask;  // ring position of the rank
-            const uint32_t korg = (k * kRT) * 8u;          // tile origin in ring bytes (mod)
-            const double* fs = stages + static_cast<size_t>(st) * p.stage_elems + t;
+            // tile k's window [k - A, k + A] starts at ring position k mod W;
+            // every neighbour source is a uniform pointer per tile (ring or stage)
+            const double* nb = ring + static_cast<size_t>(k % kRW + p.A) * kRT;
+            const double* fb = stages + static_cast<size_t>(st) * p.stage_elems;
             double acc = 0.0;
-            // in-neighbours in ascending rank: v-s_0 < ... < v-s_{D-1} < v+s_{D-1} < ... < v+s_0.
-            // The source (ring or staged far range) is a select on the address,
-            // so every load is one predicated LDS and the loads of a tile issue
-            // back to back ahead of the ordered adds (no branch per neighbour).
+            // in-neighbours in ascending rank: v-s_0 < ... < v-s_{D-1} < v+s_{D-1} < ... < v+s_0
             const double* src[2 * DIMS];
 #pragma unroll
-            for (int j = 0; j < 2 * DIMS; ++j) {
-                const int i = j < DIMS ? j : 2 * DIMS - 1 - j;
+            for (int i = 0; i < DIMS; ++i) {
                 const bool rg = (p.ring_dims >> i) & 1u;
-                src[j] = rg ? reinterpret_cast<const double*>(
-                                  reinterpret_cast<const uint8_t*>(ring) +
-                                  ((korg + roff[j]) & (kRMask * 8u + 7u)))
-                            : fs + static_cast<size_t>(j < DIMS ? p.lo_far[i] : p.hi_far[i]) * kRT;
+                src[i] = rg ? nb - s.stride[i] : fb + static_cast<size_t>(p.lo_far[i]) * kRT;
+                src[2 * DIMS - 1 - i] = rg ? nb + s.stride[i] : fb + static_cast<size_t>(p.hi_far[i]) * kRT;
             }
 #pragma unroll
             for (int j = 0; j < 2 * DIMS; ++j)
-                if ((mask >> j) & 1u) acc = __dadd_rn(acc, *src[j]);
-            const double cold = final_pass ? 0.0 : ring[rbt];
+                if ((mask >> j) & 1u) acc = __dadd_rn(acc, src[j][t]);
+            const double cold = final_pass ? 0.0 : nb[t];
             __syncwarp();
             if (lane == 0) mbar_arrive(&pp.empty[st]);  // this warp is done with the stage
             const uint32_t v = k * kRT + t;
@@ -373,8 +374,8 @@ bool make_ring_plan(const DevShape& s, int smem_budget, int num_sms, RingPlan* o
     if (p.chunk < 1) return false;
     // every CTA sweeps at least one whole chunk
     if (ntiles < static_cast<uint64_t>(num_sms) * p.chunk) return false;
-    const long long ring_bytes = static_cast<long long>(kRW) * kRT * 8;
-    // reach: the largest A with W >= 2A + S that still leaves >= 2 stages
+    // reach A: W >= 2A + S keeps every slot a consumer may still read out of the
+    // producers' way; the ring region holds W slots plus A mirror slots each side
     int best = -1;
     for (int S = kRMaxStages; S >= 2 && best < 0; --S) {
         for (int A = (kRW - S) / 2; A >= 1; --A) {
@@ -386,7 +387,8 @@ bool make_ring_plan(const DevShape& s, int smem_budget, int num_sms, RingPlan* o
                     even = even && (s.stride[i] % 2 == 0);
                 }
             if (!even) continue;  // far ranges must start 16-byte aligned
-            const long long need = ring_bytes + static_cast<long long>(S) * nfar * kRT * 8;
+            const long long need = static_cast<long long>(kRW + 2 * A) * kRT * 8 +
+                                   static_cast<long long>(S) * nfar * kRT * 8;
             if (need > smem_budget) continue;
             p.A = A;
             p.stages = S;
@@ -420,7 +422,7 @@ bool make_ring_plan(const DevShape& s, int smem_budget, int num_sms, RingPlan* o
             if (d > lim) p.far_ef |= 1u << q;
         }
     }
-    if (p.nfar + 1 + 2 * p.A > 32 * kRProdWarps) return false;
+    if (p.nfar + 2 * (2 * p.A + 1) > 32 * kRProdWarps) return false;
     *out = p;
     return true;
 }
@@ -442,7 +444,7 @@ cudaError_t launch_pagerank_ring(const DevShape& s, const PrArgs& a, int smem_bu
     if (!make_ring_plan(s, smem_budget, num_sms, &p)) return cudaErrorNotSupported;
     void* k = ring_kernel(s.dims);
     if (!k) return cudaErrorInvalidValue;
-    const size_t smem = static_cast<size_t>(kRW) * kRT * 8 +
+    const size_t smem = static_cast<size_t>(kRW + 2 * p.A) * kRT * 8 +
                         static_cast<size_t>(p.stages) * p.nfar * kRT * 8;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
