@@ -607,9 +607,17 @@ int do_load_sparse_keys(tk_land* l, const unsigned long long* dkeys, const doubl
     l->hcap = 0;
     Small* ds = l->small.as<Small>();
     TKC(cudaMemsetAsync(&ds->err, 0, 4, l->stream));
+    // TK_INGEST_PARTITION=1: pairs partitioned by table slice first, so the
+    // scatter stays in L2 (scatter 8.5 -> 3.3 ms on C5, but the partition pass
+    // costs 4.4 ms: 8.2 vs 8.7 ms in total; profiles/hash/r02_partition.md)
+    void* scratch = nullptr;
+    if (std::getenv("TK_INGEST_PARTITION") && nv) {
+        TKC(ensure(l->tmp, tk::load_valid_scratch_bytes(nv, static_cast<uint32_t>(l->n))));
+        scratch = l->tmp.p;
+    }
     TKC(tk::launch_load_valid(dkeys, dvals, nv, static_cast<uint32_t>(l->n), l->fit.as<double>(),
                               l->ok.as<uint8_t>(), l->claimed.as<unsigned int>(), &ds->err,
-                              l->stream));
+                              l->stream, scratch));
     TKC(cudaMemcpyAsync(&l->hsmall->err, &ds->err, 4, cudaMemcpyDeviceToHost, l->stream));
     TKC(cudaStreamSynchronize(l->stream));
     l->built = l->pr_done = false;

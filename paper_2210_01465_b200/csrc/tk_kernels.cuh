@@ -18,9 +18,13 @@ cudaError_t launch_encode_configs(const int32_t* configs, uint64_t n_valid, int 
                                   cudaStream_t stream);
 // valid (key, fitness) pairs -> dense rank-indexed table; err bits 1 key >= N,
 // 2 duplicate key, 4 mean >= kFailFitness.  claimed: ceil(n/32) u32 scratch.
+// scratch (load_valid_scratch_bytes, or null for the direct scatter): the pairs
+// are first partitioned by 2^17-rank slices so the scatter stays in L2
 cudaError_t launch_load_valid(const unsigned long long* keys, const double* vals,
                               uint64_t n_valid, uint32_t n, double* fit, uint8_t* ok,
-                              unsigned int* claimed, int* err_flag, cudaStream_t stream);
+                              unsigned int* claimed, int* err_flag, cudaStream_t stream,
+                              void* scratch);
+size_t load_valid_scratch_bytes(uint64_t n_valid, uint32_t n);
 // failed entries -> kFailFitness; err bit 4 if an ok mean >= kFailFitness
 cudaError_t launch_normalize_dense(uint32_t n, double* fit, const uint8_t* ok, int* err_flag,
                                    cudaStream_t stream);

@@ -137,8 +137,13 @@ def tk():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("ingest", ["direct", "partition"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_constraint_shaped_load_sparse_configs_lookup(tk, name):
+def test_constraint_shaped_load_sparse_configs_lookup(tk, monkeypatch, name, ingest):
+    """Both ingest paths: the direct scatter and the slice-partitioned one
+    (TK_INGEST_PARTITION=1)."""
+    if ingest == "partition":
+        monkeypatch.setenv("TK_INGEST_PARTITION", "1")
     radix, d, fit, ok = case_table(name)
     keys = np.flatnonzero(ok).astype(np.uint64)
     perm = np.random.default_rng(1).permutation(keys.size)
