@@ -32,6 +32,12 @@ if [[ $WHAT == all || $WHAT == bench || $WHAT == quick ]]; then
   timeout 1200 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 \
       > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
   timeout 600 python bench.py --workload c4 --steps 2 > "$OUT/bench_c4.json" 2> "$OUT/bench_c4.err"
+  # BASELINE.json configs[0] / configs[1] (C1, C2): product and reference arms
+  for w in c1 c2; do
+    timeout 600 python bench.py --workload $w --steps 10 --warmup 3 > "$OUT/bench_$w.json" 2> "$OUT/bench_$w.err"
+    timeout 600 python bench.py --workload $w --impl reference --steps 3 --warmup 1 \
+        > "$OUT/bench_ref_$w.json" 2> "$OUT/bench_ref_$w.err"
+  done
   # N=2 without a launcher: bench.py re-executes itself under torch.distributed.run;
   # on the one-GPU box both ranks share the device over gloo (CUDA IPC peers)
   TK_FORCE_DEVICE=0 TK_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 2 \
