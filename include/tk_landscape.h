@@ -157,6 +157,35 @@ int tk_analyze(tk_land* land, int kind, double damping, double tol, int64_t max_
                uint64_t node_limit, int p_max_percent, int emit_csr,
                tk_report_summary* out);
 
+/* ---------------------------------------- batches of small spaces (C4) -- */
+/* analyze_landscape (landscape.hpp:77-79) for many small spaces in one call:
+ * one upload, one launch (one CTA per space runs FFG, f_opt, minima, PageRank,
+ * C_p and the report rows), one read-back.  For N <= 2^20 configurations and
+ * <= 64 neighbour slots per space; other items get status TK_EINVAL.  fitness
+ * / ok are host (TK_MEM_HOST) or device (TK_MEM_DEVICE) pointers per item;
+ * the minima_* outputs are host pointers with room for minima_capacity rows
+ * (NULL: no rows).  Per-item results in summary and status (TK_OK,
+ * TK_ENOFEAS, TK_ENOCONV, TK_EDEGEN, TK_EINVAL); the call itself returns
+ * TK_OK unless the arguments or the device fail.  The global sums are block
+ * reductions, so per-node ranks can differ from tk_analyze's in the last bits
+ * (its dangling mass is summed in another order); both are checked against
+ * the oracle. */
+typedef struct tk_batch_item {
+    uint32_t dims;
+    uint32_t radix[TK_MAX_DIMS];
+    const double* fitness;
+    const uint8_t* ok;
+    uint64_t* minima_ranks;
+    double* minima_fitness;
+    double* minima_fraction;
+    double* minima_pagerank;
+    uint64_t minima_capacity;
+    tk_report_summary summary;
+    int32_t status;
+} tk_batch_item;
+int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kind, double damping,
+                     double tol, int64_t max_iter, int p_max_percent, int mem);
+
 /* ------------------------------- random-walk validator -- */
 /* hillclimb.cpp:48-87 climb_random_first, batched on the device: `walkers`
  * randomized first-improvement descents from uniform starts over the loaded

@@ -27,7 +27,7 @@ EXPORTS = [
     "tk_land_generate", "tk_land_copy_fitness", "tk_land_lookup", "tk_optimum",
     "tk_ffg_build", "tk_ffg_copy_out", "tk_census", "tk_pagerank",
     "tk_pagerank_copy_out", "tk_centrality", "tk_report_copy_out", "tk_analyze",
-    "tk_pagerank_csr", "tk_proportion_of_centrality", "tk_descents",
+    "tk_pagerank_csr", "tk_proportion_of_centrality", "tk_descents", "tk_batch_analyze",
     "tk_land_set_shard", "tk_land_replica_ptrs", "tk_land_set_peer_ptrs", "tk_land_ipc_handles",
     "tk_land_open_peers", "tk_shard_optimum", "tk_shard_pagerank_init", "tk_shard_pagerank_step",
     "tk_shard_pagerank_init_dev", "tk_shard_pagerank_step_dev", "tk_shard_pagerank_rewind",
@@ -43,6 +43,17 @@ class ReportSummary(C.Structure):
         ("c_p", C.c_double * TK_MAX_CP),
         ("ms_load", C.c_float), ("ms_ffg", C.c_float), ("ms_pagerank", C.c_float),
         ("ms_centrality", C.c_float),
+    ]
+
+
+class BatchItem(C.Structure):
+    """tk_batch_item (include/tk_landscape.h)."""
+    _fields_ = [
+        ("dims", C.c_uint32), ("radix", C.c_uint32 * 32),
+        ("fitness", C.c_void_p), ("ok", C.c_void_p),
+        ("minima_ranks", C.c_void_p), ("minima_fitness", C.c_void_p),
+        ("minima_fraction", C.c_void_p), ("minima_pagerank", C.c_void_p),
+        ("minima_capacity", C.c_uint64), ("summary", ReportSummary), ("status", C.c_int32),
     ]
 
 
@@ -85,6 +96,7 @@ def load(path: str = LIB_PATH):
         "tk_ffg_copy_out": (I, [P, P, P, P, P]),
         "tk_census": (I, [P, PU64, PU64, PU64, P]),
         "tk_descents": (I, [P, C.c_uint64, C.c_uint64, I, P, PU64, PU64]),
+        "tk_batch_analyze": (I, [I, P, C.c_uint32, I, D, D, C.c_int64, I, I]),
         "tk_pagerank": (I, [P, D, D, C.c_int64, PI64, PD, PD]),
         "tk_pagerank_copy_out": (I, [P, P]),
         "tk_centrality": (I, [P, D, P, I, P]),

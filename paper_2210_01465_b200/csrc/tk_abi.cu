@@ -1125,6 +1125,164 @@ int tk_analyze(tk_land* l, int kind, double damping, double tol, int64_t max_ite
     TK_GUARD_END
 }
 
+// ---------------------------------------------- batches of small spaces --
+
+namespace {
+// per-device batch context: one stream, a device workspace and a pinned
+// read-back buffer, reused across calls (guarded: one batch at a time per device)
+struct BatchCtx {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    DevBuf ws;
+    void* host_out = nullptr;
+    size_t host_out_cap = 0;
+};
+BatchCtx& batch_ctx(int device) {
+    static BatchCtx ctx[64];
+    return ctx[device & 63];
+}
+}  // namespace
+
+int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kind, double damping,
+                     double tol, int64_t max_iter, int p_max_percent, int mem) {
+    if (!items && n_items) return fail(TK_EINVAL, "batch_analyze: null items");
+    if (kind != TK_ADJACENT && kind != TK_HAMMING) return fail(TK_EINVAL, "batch_analyze: kind");
+    if (p_max_percent < 0 || p_max_percent >= TK_MAX_CP)
+        return fail(TK_EINVAL, "batch_analyze: p_max_percent must be in [0, 100]");
+    if (int st = check_pr_args(damping, tol, max_iter)) return st;
+    if (n_items == 0) return TK_OK;
+    TK_GUARD_BEGIN
+    BatchCtx& C = batch_ctx(device);
+    std::lock_guard<std::mutex> lk(C.mu);
+    TKC(cudaSetDevice(device));
+    if (!C.init) {
+        TKC(cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking));
+        TKC(cudaDeviceGetAttribute(&C.num_sms, cudaDevAttrMultiProcessorCount, device));
+        C.init = true;
+    }
+    // workspace layout: [descs][outs][per item: fitness, ok, scratch, report rows]
+    const size_t dsz = tk::batch_desc_bytes();
+    auto a256 = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    std::vector<uint64_t> ns(n_items, 0);
+    std::vector<size_t> off(n_items, 0);
+    size_t total = a256(dsz * n_items) + a256(sizeof(tk::BatchOut) * n_items);
+    for (uint32_t i = 0; i < n_items; ++i) {
+        items[i].status = TK_OK;
+        std::memset(&items[i].summary, 0, sizeof(items[i].summary));
+        if (items[i].dims < 1 || items[i].dims > TK_MAX_DIMS ||
+            !tk::batch_item_supported(items[i].dims, items[i].radix, kind, &ns[i]) ||
+            !items[i].fitness || !items[i].ok) {
+            items[i].status = TK_EINVAL;
+            ns[i] = 0;
+            continue;
+        }
+        off[i] = total;
+        total += a256(8 * ns[i]) + a256(ns[i]) +
+                 tk::batch_workspace_bytes(static_cast<uint32_t>(ns[i]),
+                                           tk::batch_slots(items[i].dims, items[i].radix, kind)) +
+                 4 * a256(8 * ns[i]);
+    }
+    TKC(ensure(C.ws, total));
+    uint8_t* base = C.ws.as<uint8_t>();
+    tk::BatchOut* dout = reinterpret_cast<tk::BatchOut*>(base + a256(dsz * n_items));
+    std::vector<uint8_t> descs(dsz * n_items, 0);
+    std::vector<uint32_t> live;
+    for (uint32_t i = 0; i < n_items; ++i) {
+        if (!ns[i]) continue;
+        uint8_t* p = base + off[i];
+        const uint64_t n = ns[i];
+        double* fit = reinterpret_cast<double*>(p);
+        uint8_t* ok = p + a256(8 * n);
+        uint8_t* scr = ok + a256(n);
+        const uint32_t slots = tk::batch_slots(items[i].dims, items[i].radix, kind);
+        uint8_t* rows = scr + tk::batch_workspace_bytes(static_cast<uint32_t>(n), slots);
+        const double* fsrc = items[i].fitness;
+        const uint8_t* osrc = items[i].ok;
+        if (mem == TK_MEM_DEVICE) {
+            fit = const_cast<double*>(fsrc);
+            ok = const_cast<uint8_t*>(osrc);
+        } else {
+            TKC(cudaMemcpyAsync(fit, fsrc, 8 * n, cudaMemcpyHostToDevice, C.stream));
+            TKC(cudaMemcpyAsync(ok, osrc, n, cudaMemcpyHostToDevice, C.stream));
+        }
+        unsigned long long* rr = reinterpret_cast<unsigned long long*>(rows);
+        double* rf = reinterpret_cast<double*>(rows + a256(8 * n));
+        double* rq = reinterpret_cast<double*>(rows + 2 * a256(8 * n));
+        double* rp = reinterpret_cast<double*>(rows + 3 * a256(8 * n));
+        const bool want_rows = items[i].minima_ranks || items[i].minima_fitness ||
+                               items[i].minima_fraction || items[i].minima_pagerank;
+        tk::batch_fill_desc(descs.data() + dsz * live.size(), fit, ok, static_cast<uint32_t>(n),
+                            slots, items[i].dims, items[i].radix, scr, dout + live.size(),
+                            want_rows ? rr : nullptr, rf, rq, rp);
+        live.push_back(i);
+    }
+    if (live.empty()) return TK_OK;
+    const uint32_t nl = static_cast<uint32_t>(live.size());
+    TKC(cudaMemcpyAsync(base, descs.data(), dsz * nl, cudaMemcpyHostToDevice, C.stream));
+    tk::BatchParams P{};
+    P.kind = kind;
+    P.damping = damping;
+    P.tol = tol;
+    P.max_iter = max_iter;
+    P.n_p = p_max_percent + 1;
+    for (int k = 0; k < P.n_p; ++k) {
+        const double pk = k / 100.0;
+        P.onep[k] = 1.0 + pk;  // the band of launch_centrality: f < (1 + p) * f_opt
+        P.zero[k] = pk == 0.0;
+    }
+    TKC(tk::launch_batch_analyze(base, nl, P, C.num_sms, C.stream));
+    const size_t ob = sizeof(tk::BatchOut) * nl;
+    if (C.host_out_cap < ob) {
+        if (C.host_out) cudaFreeHost(C.host_out);
+        C.host_out = nullptr;
+        C.host_out_cap = 0;
+        TKC(cudaMallocHost(&C.host_out, ob));
+        C.host_out_cap = ob;
+    }
+    TKC(cudaMemcpyAsync(C.host_out, dout, ob, cudaMemcpyDeviceToHost, C.stream));
+    TKC(cudaStreamSynchronize(C.stream));
+    const tk::BatchOut* ho = static_cast<const tk::BatchOut*>(C.host_out);
+    for (uint32_t j = 0; j < nl; ++j) {
+        tk_batch_item& it = items[live[j]];
+        const tk::BatchOut& o = ho[j];
+        tk_report_summary& s = it.summary;
+        s.n_nodes = o.n_nodes;
+        s.n_edges = o.n_edges;
+        s.n_minima = o.n_minima;
+        s.f_opt = o.f_opt;
+        s.opt_rank = o.opt_rank;
+        s.iterations = o.iterations;
+        s.residual = o.residual;
+        s.pagerank_sum = o.pagerank_sum;
+        s.n_cp = P.n_p;
+        for (int k = 0; k < P.n_p; ++k) s.c_p[k] = o.c_p[k];
+        it.status = o.status;
+        const uint64_t m = std::min<uint64_t>(o.n_minima, it.minima_capacity);
+        if (o.status != TK_OK || !m) continue;
+        const uint64_t n = ns[live[j]];
+        const tk_batch_item& src_it = items[live[j]];
+        uint8_t* rows = base + off[live[j]] + a256(8 * n) + a256(n) +
+                        tk::batch_workspace_bytes(static_cast<uint32_t>(n),
+                                                  tk::batch_slots(src_it.dims, src_it.radix, kind));
+        if (it.minima_ranks)
+            TKC(cudaMemcpyAsync(it.minima_ranks, rows, m * 8, cudaMemcpyDeviceToHost, C.stream));
+        if (it.minima_fitness)
+            TKC(cudaMemcpyAsync(it.minima_fitness, rows + a256(8 * n), m * 8, cudaMemcpyDeviceToHost,
+                                C.stream));
+        if (it.minima_fraction)
+            TKC(cudaMemcpyAsync(it.minima_fraction, rows + 2 * a256(8 * n), m * 8,
+                                cudaMemcpyDeviceToHost, C.stream));
+        if (it.minima_pagerank)
+            TKC(cudaMemcpyAsync(it.minima_pagerank, rows + 3 * a256(8 * n), m * 8,
+                                cudaMemcpyDeviceToHost, C.stream));
+    }
+    TKC(cudaStreamSynchronize(C.stream));
+    return TK_OK;
+    TK_GUARD_END
+}
+
 // ------------------------------------------------ random-walk validator --
 
 int tk_descents(tk_land* l, uint64_t walkers, uint64_t seed, int restart_scan,

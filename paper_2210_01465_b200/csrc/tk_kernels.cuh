@@ -288,6 +288,36 @@ cudaError_t launch_report(const uint32_t* minima, uint64_t m, const double* fit,
 cudaError_t launch_gather_values(const uint32_t* idx, uint64_t m, const double* src,
                                  double* dst, cudaStream_t stream);
 
+// ---- batches of small spaces (tk_batch.cu) --------------------------------------
+constexpr uint64_t kBatchMaxNodes = 1ull << 20;
+struct BatchOut {
+    unsigned long long n_nodes, n_edges, n_minima, opt_rank;
+    double f_opt;
+    long long iterations;
+    double residual, pagerank_sum;
+    double c_p[TK_MAX_CP];
+    int status;
+};
+struct BatchParams {
+    int kind;
+    double damping, tol;
+    long long max_iter;
+    int n_p;
+    double onep[TK_MAX_CP];  // 1 + p (host IEEE), the band f < (1 + p) f_opt
+    int zero[TK_MAX_CP];     // p == 0: f <= f_opt
+};
+bool batch_item_supported(uint32_t dims, const uint32_t* radix, int kind, uint64_t* n_out);
+size_t batch_desc_bytes();
+size_t batch_workspace_bytes(uint32_t n, uint32_t slots);
+uint32_t batch_slots(uint32_t dims, const uint32_t* radix, int kind);
+void batch_fill_desc(void* desc_host, const double* fit, const uint8_t* ok, uint32_t n,
+                     uint32_t slots, uint32_t dims_in, const uint32_t* radix_in, uint8_t* ws,
+                     BatchOut* out,
+                     unsigned long long* rep_rank, double* rep_fit, double* rep_frac,
+                     double* rep_pr);
+cudaError_t launch_batch_analyze(const void* descs_dev, uint32_t n_items, const BatchParams& P,
+                                 int num_sms, cudaStream_t stream);
+
 // ---- random-walk validator (tk_descent.cu) ------------------------------------
 constexpr int kMaxDescentSlots = 256;
 struct DescentArgs {

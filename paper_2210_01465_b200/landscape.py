@@ -17,6 +17,7 @@ on the GPU through libtk_landscape.so; nothing here computes on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -529,6 +530,7 @@ class BatchAnalyzer:
         from concurrent.futures import ThreadPoolExecutor
 
         self.workers = max(1, int(workers))
+        self.device = device
         self.lands = [Landscape(list(radix0), device) for _ in range(self.workers)]
         self.pool = ThreadPoolExecutor(self.workers)
 
@@ -544,6 +546,63 @@ class BatchAnalyzer:
         self.close()
 
     def run(self, items, kind: int, reports=None, **analyze_kw):
+        """Analyse every item.  Spaces of <= 2^20 configurations (and <= 64
+        neighbour slots) go through one tk_batch_analyze call -- one upload, one
+        launch with one CTA per space, one read-back; others (or
+        TK_BATCH_THREADS=1, or emit_csr) through the worker threads."""
+        if not analyze_kw.get("emit_csr") and not os.environ.get("TK_BATCH_THREADS"):
+            got = self._run_batched(items, kind, reports, **analyze_kw)
+            if got is not None:
+                return got
+        return self._run_threads(items, kind, reports, **analyze_kw)
+
+    def _run_batched(self, items, kind, reports, damping=0.85, tol=1e-10, max_iter=100000,
+                     node_limit=1_000_000, p_max_percent=15, emit_csr=False):
+        n = len(items)
+        arr = (_abi.BatchItem * max(1, n))()
+        for k, (radix, fp, op) in enumerate(items):
+            radix = [int(m) for m in radix]
+            size = int(np.prod(radix, dtype=np.int64))
+            slots = sum((2 if kind == ADJACENT else m - 1) for m in radix if m >= 2)
+            if size > (1 << 20) or slots > 64 or len(radix) > 32:
+                return None
+            if size > node_limit:
+                raise InvalidArgument(f"node_limit {node_limit} below the space size {size}")
+            it = arr[k]
+            it.dims = len(radix)
+            for i, m in enumerate(radix):
+                it.radix[i] = m
+            it.fitness, it.ok = fp, op
+            if reports is not None and reports[k] is not None:
+                (it.minima_ranks, it.minima_fitness, it.minima_fraction,
+                 it.minima_pagerank) = reports[k]
+                it.minima_capacity = (1 << 62)
+        L = _abi.load()
+        _check(L.tk_batch_analyze(self.device, arr, n, kind, damping, tol, max_iter,
+                                  p_max_percent, _abi.TK_MEM_HOST))
+        out = []
+        for k in range(n):
+            it = arr[k]
+            st = it.status
+            if st != _abi.TK_OK:
+                s = it.summary
+                msgs = {_abi.TK_ENOFEAS: "no feasible point (every configuration failed)",
+                        _abi.TK_ENOCONV: f"pagerank did not converge in {s.iterations} iterations",
+                        _abi.TK_EDEGEN: "proportion_of_centrality: minima hold zero PageRank mass",
+                        _abi.TK_EINVAL: "space not supported by the batch path"}
+                if st == _abi.TK_ENOFEAS:
+                    raise NoFeasiblePoint(msgs[st])
+                if st == _abi.TK_ENOCONV:
+                    raise NonConvergence(msgs[st], s.iterations, s.residual)
+                if st == _abi.TK_EINVAL:
+                    raise InvalidArgument(msgs[st])
+                raise Error(msgs.get(st, f"status {st}"))
+            s = _abi.ReportSummary()
+            C.pointer(s)[0] = it.summary
+            out.append(s)
+        return out
+
+    def _run_threads(self, items, kind: int, reports=None, **analyze_kw):
         import threading
 
         out = [None] * len(items)

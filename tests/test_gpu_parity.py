@@ -453,35 +453,55 @@ def test_analysis_pipeline_matches_single_handle(tk):
             assert np.array_equal(a[: w[2]], b)
 
 
-def test_batch_analyzer_concurrent_handles_match_sequential(tk):
-    """tk.BatchAnalyzer (several handles / streams in flight, cooperative
-    PageRank grids admitted concurrently by SM footprint) returns what one
-    handle analysing the spaces one after another returns."""
+@pytest.mark.parametrize("path", ["batched", "threads"])
+@pytest.mark.parametrize("kind", [O.ADJACENT, O.HAMMING])
+def test_batch_analyzer_matches_oracle(tk, monkeypatch, path, kind):
+    """tk.BatchAnalyzer on both of its paths -- one tk_batch_analyze launch with
+    one CTA per space, and worker threads driving several handles / streams --
+    against the oracle: iterations, edges and minima exact, C_p within 1e-9,
+    report rows (ranks, fitness, fraction of optimum) exact and the minima's
+    PageRank within 1e-12."""
+    if path == "threads":
+        monkeypatch.setenv("TK_BATCH_THREADS", "1")
     shapes = [[8, 6, 3, 3, 2], [12, 6, 8, 8, 2, 2], [4, 4, 3, 3, 3, 3, 4, 4, 2, 2],
-              [31, 11, 4, 2, 3], [6, 5, 4, 3, 2, 2, 2]]
+              [31, 11, 4, 2, 3], [6, 5, 4, 3, 2, 2, 2], [7, 1, 5], [2, 2]]
     tables = []
     for k, radix in enumerate(shapes * 2):
         fit, ok = O.gen_synthetic(radix, 0.1 * (k % 5), "rugged", k)
         tables.append((radix, np.ascontiguousarray(fit, np.float64),
                        np.ascontiguousarray(ok, np.uint8)))
-    want = []
-    for radix, fit, ok in tables:
-        with tk.Landscape(radix) as land:
-            land.load_dense(fit, ok)
-            s = land.analyze(tk.ADJACENT, node_limit=1 << 32)
-            want.append((s.iterations, s.n_edges, s.n_minima, list(s.c_p[:16]),
-                         land.report_rows(s.f_opt)))
-    bufs = [[np.empty(max(1, w[2]), dt) for dt in (np.uint64, np.float64, np.float64,
-                                                   np.float64)] for w in want]
+    refs = [O.analyze(radix, fit, ok, kind, node_limit=1 << 32) for radix, fit, ok in tables]
+    bufs = [[np.empty(max(1, len(r["ffg"]["minima"])), dt) for dt in (np.uint64, np.float64,
+                                                                    np.float64, np.float64)]
+            for r in refs]
     items = [(radix, f.ctypes.data, o.ctypes.data) for radix, f, o in tables]
     with tk.BatchAnalyzer(workers=4) as batch:
-        got = batch.run(items, tk.ADJACENT, [tuple(b.ctypes.data for b in bb) for bb in bufs],
+        got = batch.run(items, kind, [tuple(b.ctypes.data for b in bb) for bb in bufs],
                         node_limit=1 << 32)
-    for s, w, bb in zip(got, want, bufs):
-        assert (s.iterations, s.n_edges, s.n_minima) == w[:3]
-        assert list(s.c_p[:16]) == w[3]
-        for a, b in zip(bb, w[4]):
-            assert np.array_equal(a[: w[2]], b)
+    for (radix, fit, ok), s, ref, bb in zip(tables, got, refs, bufs):
+        g = ref["ffg"]
+        mins = g["minima"]
+        assert s.iterations == ref["iterations"], radix
+        assert s.n_edges == len(g["targets"]) and s.n_minima == len(mins)
+        assert s.f_opt == fit[ok.astype(bool)].min()
+        for k, c in ref["c_p_curve"]:
+            assert abs(s.c_p[k] - c) <= CP_ATOL
+        ranks, fmin, frac, prm = (b[: len(mins)] for b in bb)
+        assert np.array_equal(ranks, mins.astype(np.uint64))
+        assert np.array_equal(fmin.view(np.uint64), fit[mins].view(np.uint64))
+        assert np.array_equal(frac, fit[ok.astype(bool)].min() / fit[mins])
+        assert np.max(np.abs(prm - ref["pagerank"][mins]), initial=0.0) <= 1e-12
+
+
+def test_batch_analyze_statuses(tk):
+    """Per-item statuses of the batched path: a space whose configurations all
+    failed raises NoFeasiblePoint (errors.hpp:32-35), like analyze_landscape."""
+    radix = [4, 3]
+    fit = np.full(12, 1e10)
+    ok = np.zeros(12, np.uint8)
+    with tk.BatchAnalyzer() as batch:
+        with pytest.raises(tk.NoFeasiblePoint):
+            batch.run([(radix, fit.ctypes.data, ok.ctypes.data)], O.ADJACENT)
 
 
 @pytest.mark.slow
