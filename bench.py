@@ -171,6 +171,7 @@ def run_batch(args, wl, kind):
         edges = float(e.item())
     ms_step = t_ms / args.steps
     pr_ms = float(np.mean([s.ms_pagerank for s in runs[-1]]))
+    threaded = bool(os.environ.get("TK_BATCH_THREADS"))
     if rank == 0:
         print(json.dumps({
             "metric": "FFG+PageRank GTEPS", "value": round(edges / (t_ms / 1e3) / 1e9, 3),
@@ -183,15 +184,19 @@ def run_batch(args, wl, kind):
                        "host_workers": workers,
                        "l2": "small landscapes; host upload per landscape inside the step"},
             "s_per_space": round(ms_step / 1e3 / n_lands, 7),
-            "pagerank_kernel_ms_mean": round(pr_ms, 4),
+            "pagerank_kernel_ms_mean": round(pr_ms, 4) if threaded else None,
             "roofline": None,
             "cpu_baseline": None,
             "e2e": {"value": round(edges / (t_ms / 1e3) / 1e9, 3), "unit": "GTEPS",
                     "h2d_bytes_per_step": int(sum(9 * int(np.prod(it[0])) for it in items)),
                     "d2h_bytes_per_step": int(sum(32 * s.n_minima for s in runs[-1]) * world),
                     "note": "the step itself is end to end: host upload + report per landscape "
-                            "(tk.BatchAnalyzer: concurrent handles/streams)"},
-            "gpu_launches": int(n_lands * 9 * args.steps),
+                            + ("(tk.BatchAnalyzer: concurrent handles/streams)" if threaded else
+                               "(tk.BatchAnalyzer -> tk_batch_analyze: one upload, one launch "
+                               "with one CTA per landscape, one read-back)")},
+            "batch_path": "threads" if threaded else "batched",
+            # threads: ~9 kernels per landscape; batched: one batch_analyze_kernel per step
+            "gpu_launches": int(n_lands * 9 * args.steps) if threaded else int(args.steps),
         }))
     batch.close()
     if dist is not None:
