@@ -1135,9 +1135,11 @@ struct BatchCtx {
     bool init = false;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
-    DevBuf ws;
+    DevBuf ws, jobs;
     void* host_out = nullptr;
     size_t host_out_cap = 0;
+    void* host_rows = nullptr;
+    size_t host_rows_cap = 0;
 };
 BatchCtx& batch_ctx(int device) {
     static BatchCtx ctx[64];
@@ -1167,7 +1169,10 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
     auto a256 = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
     std::vector<uint64_t> ns(n_items, 0);
     std::vector<size_t> off(n_items, 0);
-    size_t total = a256(dsz * n_items) + a256(sizeof(tk::BatchOut) * n_items);
+    const size_t gsb = tk::batch_group_state_bytes();
+    uint64_t rows_cap = 0;  // report rows of all spaces, packed (<= sum of N)
+    size_t total = a256(dsz * n_items) + a256(sizeof(tk::BatchOut) * n_items) +
+                   a256(gsb * n_items);
     for (uint32_t i = 0; i < n_items; ++i) {
         items[i].status = TK_OK;
         std::memset(&items[i].summary, 0, sizeof(items[i].summary));
@@ -1181,12 +1186,17 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
         off[i] = total;
         total += a256(8 * ns[i]) + a256(ns[i]) +
                  tk::batch_workspace_bytes(static_cast<uint32_t>(ns[i]),
-                                           tk::batch_slots(items[i].dims, items[i].radix, kind)) +
-                 4 * a256(8 * ns[i]);
+                                           tk::batch_slots(items[i].dims, items[i].radix, kind));
+        rows_cap += ns[i];
     }
+    const size_t rows_at = total;
+    total += 256 + a256(32 * rows_cap);  // row cursor, then the rows
     TKC(ensure(C.ws, total));
     uint8_t* base = C.ws.as<uint8_t>();
+    unsigned long long* row_cursor = reinterpret_cast<unsigned long long*>(base + rows_at);
+    double* rows_dev = reinterpret_cast<double*>(base + rows_at + 256);
     tk::BatchOut* dout = reinterpret_cast<tk::BatchOut*>(base + a256(dsz * n_items));
+    uint8_t* gstate = base + a256(dsz * n_items) + a256(sizeof(tk::BatchOut) * n_items);
     std::vector<uint8_t> descs(dsz * n_items, 0);
     std::vector<uint32_t> live;
     for (uint32_t i = 0; i < n_items; ++i) {
@@ -1197,30 +1207,26 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
         uint8_t* ok = p + a256(8 * n);
         uint8_t* scr = ok + a256(n);
         const uint32_t slots = tk::batch_slots(items[i].dims, items[i].radix, kind);
-        uint8_t* rows = scr + tk::batch_workspace_bytes(static_cast<uint32_t>(n), slots);
-        const double* fsrc = items[i].fitness;
-        const uint8_t* osrc = items[i].ok;
         if (mem == TK_MEM_DEVICE) {
-            fit = const_cast<double*>(fsrc);
-            ok = const_cast<uint8_t*>(osrc);
+            fit = const_cast<double*>(items[i].fitness);
+            ok = const_cast<uint8_t*>(items[i].ok);
         } else {
-            TKC(cudaMemcpyAsync(fit, fsrc, 8 * n, cudaMemcpyHostToDevice, C.stream));
-            TKC(cudaMemcpyAsync(ok, osrc, n, cudaMemcpyHostToDevice, C.stream));
+            TKC(cudaMemcpyAsync(fit, items[i].fitness, 8 * n, cudaMemcpyHostToDevice, C.stream));
+            TKC(cudaMemcpyAsync(ok, items[i].ok, n, cudaMemcpyHostToDevice, C.stream));
         }
-        unsigned long long* rr = reinterpret_cast<unsigned long long*>(rows);
-        double* rf = reinterpret_cast<double*>(rows + a256(8 * n));
-        double* rq = reinterpret_cast<double*>(rows + 2 * a256(8 * n));
-        double* rp = reinterpret_cast<double*>(rows + 3 * a256(8 * n));
         const bool want_rows = items[i].minima_ranks || items[i].minima_fitness ||
                                items[i].minima_fraction || items[i].minima_pagerank;
         tk::batch_fill_desc(descs.data() + dsz * live.size(), fit, ok, static_cast<uint32_t>(n),
-                            slots, items[i].dims, items[i].radix, scr, dout + live.size(),
-                            want_rows ? rr : nullptr, rf, rq, rp);
+                            slots, items[i].dims, items[i].radix, scr,
+                            reinterpret_cast<unsigned int*>(gstate + gsb * live.size()),
+                            reinterpret_cast<double*>(gstate + gsb * live.size() + 64),
+                            dout + live.size(), want_rows ? rows_dev : nullptr, row_cursor);
         live.push_back(i);
     }
     if (live.empty()) return TK_OK;
     const uint32_t nl = static_cast<uint32_t>(live.size());
     TKC(cudaMemcpyAsync(base, descs.data(), dsz * nl, cudaMemcpyHostToDevice, C.stream));
+    TKC(cudaMemsetAsync(row_cursor, 0, 8, C.stream));
     tk::BatchParams P{};
     P.kind = kind;
     P.damping = damping;
@@ -1232,7 +1238,52 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
         P.onep[k] = 1.0 + pk;  // the band of launch_centrality: f < (1 + p) * f_opt
         P.zero[k] = pk == 0.0;
     }
-    TKC(tk::launch_batch_analyze(base, nl, P, C.num_sms, C.stream));
+    const int R = tk::batch_group_resident(C.num_sms);
+    const bool grouped = R > 0 && P.n_p <= tk::batch_group_max_np() && !std::getenv("TK_BATCH_NOGROUP");
+    if (grouped) {
+        // spaces largest first; a space of n ranks gets ceil(n / 8192) CTAs (at
+        // most batch_group_max); jobs dealt into waves of R CTAs, a space's
+        // members in one wave
+        std::vector<uint32_t> order(nl);
+        for (uint32_t j = 0; j < nl; ++j) order[j] = j;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t a, uint32_t b) { return ns[live[a]] > ns[live[b]]; });
+        std::vector<int> gsz(nl);
+        for (uint32_t j = 0; j < nl; ++j) {
+            const uint64_t g = (ns[live[j]] + 8191) / 8192;
+            gsz[j] = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(g, 1),
+                                                         std::min(tk::batch_group_max(), R)));
+        }
+        std::vector<std::vector<std::pair<int, int>>> waves;  // per wave: (item, g) placed
+        std::vector<int> fill;
+        for (uint32_t oi : order) {
+            const int g = gsz[oi];
+            size_t w = 0;
+            while (w < waves.size() && fill[w] + g > R) ++w;
+            if (w == waves.size()) {
+                waves.emplace_back();
+                fill.push_back(0);
+            }
+            waves[w].push_back({static_cast<int>(oi), g});
+            fill[w] += g;
+        }
+        const int nw = static_cast<int>(waves.size());
+        std::vector<uint8_t> jobs(tk::batch_job_bytes() * static_cast<size_t>(nw) * R);
+        for (int w = 0; w < nw; ++w) {
+            int cta = 0;
+            for (const auto& ig : waves[w])
+                for (int r = 0; r < ig.second; ++r)
+                    tk::batch_set_job(jobs.data(), static_cast<size_t>(w) * R + cta++, ig.first, r,
+                                      ig.second);
+            for (; cta < R; ++cta) tk::batch_set_job(jobs.data(), static_cast<size_t>(w) * R + cta, -1, 0, 1);
+        }
+        TKC(ensure(C.jobs, jobs.size()));
+        TKC(cudaMemcpyAsync(C.jobs.p, jobs.data(), jobs.size(), cudaMemcpyHostToDevice, C.stream));
+        TKC(cudaMemsetAsync(gstate, 0, gsb * nl, C.stream));  // group barriers start at {0, 0}
+        TKC(tk::launch_batch_group(base, C.jobs.p, nw, R, P, C.stream));
+    } else {
+        TKC(tk::launch_batch_analyze(base, nl, P, C.num_sms, C.stream));
+    }
     const size_t ob = sizeof(tk::BatchOut) * nl;
     if (C.host_out_cap < ob) {
         if (C.host_out) cudaFreeHost(C.host_out);
@@ -1242,8 +1293,22 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
         C.host_out_cap = ob;
     }
     TKC(cudaMemcpyAsync(C.host_out, dout, ob, cudaMemcpyDeviceToHost, C.stream));
+    unsigned long long n_rows = 0;
+    TKC(cudaMemcpyAsync(&n_rows, row_cursor, 8, cudaMemcpyDeviceToHost, C.stream));
+    TKC(cudaStreamSynchronize(C.stream));
+    // the packed report rows: one read-back into pinned staging
+    const size_t rb = static_cast<size_t>(n_rows) * 32;
+    if (C.host_rows_cap < rb) {
+        if (C.host_rows) cudaFreeHost(C.host_rows);
+        C.host_rows = nullptr;
+        C.host_rows_cap = 0;
+        TKC(cudaMallocHost(&C.host_rows, rb));
+        C.host_rows_cap = rb;
+    }
+    if (rb) TKC(cudaMemcpyAsync(C.host_rows, rows_dev, rb, cudaMemcpyDeviceToHost, C.stream));
     TKC(cudaStreamSynchronize(C.stream));
     const tk::BatchOut* ho = static_cast<const tk::BatchOut*>(C.host_out);
+    const double* hrows = static_cast<const double*>(C.host_rows);
     for (uint32_t j = 0; j < nl; ++j) {
         tk_batch_item& it = items[live[j]];
         const tk::BatchOut& o = ho[j];
@@ -1261,22 +1326,13 @@ int tk_batch_analyze(int device, tk_batch_item* items, uint32_t n_items, int kin
         it.status = o.status;
         const uint64_t m = std::min<uint64_t>(o.n_minima, it.minima_capacity);
         if (o.status != TK_OK || !m) continue;
-        const uint64_t n = ns[live[j]];
-        const tk_batch_item& src_it = items[live[j]];
-        uint8_t* rows = base + off[live[j]] + a256(8 * n) + a256(n) +
-                        tk::batch_workspace_bytes(static_cast<uint32_t>(n),
-                                                  tk::batch_slots(src_it.dims, src_it.radix, kind));
-        if (it.minima_ranks)
-            TKC(cudaMemcpyAsync(it.minima_ranks, rows, m * 8, cudaMemcpyDeviceToHost, C.stream));
-        if (it.minima_fitness)
-            TKC(cudaMemcpyAsync(it.minima_fitness, rows + a256(8 * n), m * 8, cudaMemcpyDeviceToHost,
-                                C.stream));
-        if (it.minima_fraction)
-            TKC(cudaMemcpyAsync(it.minima_fraction, rows + 2 * a256(8 * n), m * 8,
-                                cudaMemcpyDeviceToHost, C.stream));
-        if (it.minima_pagerank)
-            TKC(cudaMemcpyAsync(it.minima_pagerank, rows + 3 * a256(8 * n), m * 8,
-                                cudaMemcpyDeviceToHost, C.stream));
+        const double* row = hrows + o.row_base * 4;
+        for (uint64_t i = 0; i < m; ++i, row += 4) {
+            if (it.minima_ranks) std::memcpy(it.minima_ranks + i, row, 8);
+            if (it.minima_fitness) it.minima_fitness[i] = row[1];
+            if (it.minima_fraction) it.minima_fraction[i] = row[2];
+            if (it.minima_pagerank) it.minima_pagerank[i] = row[3];
+        }
     }
     TKC(cudaStreamSynchronize(C.stream));
     return TK_OK;

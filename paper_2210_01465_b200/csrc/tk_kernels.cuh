@@ -292,6 +292,7 @@ cudaError_t launch_gather_values(const uint32_t* idx, uint64_t m, const double* 
 constexpr uint64_t kBatchMaxNodes = 1ull << 20;
 struct BatchOut {
     unsigned long long n_nodes, n_edges, n_minima, opt_rank;
+    unsigned long long row_base;  // first row of this space's report rows (compact region)
     double f_opt;
     long long iterations;
     double residual, pagerank_sum;
@@ -312,11 +313,18 @@ size_t batch_workspace_bytes(uint32_t n, uint32_t slots);
 uint32_t batch_slots(uint32_t dims, const uint32_t* radix, int kind);
 void batch_fill_desc(void* desc_host, const double* fit, const uint8_t* ok, uint32_t n,
                      uint32_t slots, uint32_t dims_in, const uint32_t* radix_in, uint8_t* ws,
-                     BatchOut* out,
-                     unsigned long long* rep_rank, double* rep_fit, double* rep_frac,
-                     double* rep_pr);
+                     unsigned int* bar, double* part, BatchOut* out, double* rows,
+                     unsigned long long* row_cursor);
 cudaError_t launch_batch_analyze(const void* descs_dev, uint32_t n_items, const BatchParams& P,
                                  int num_sms, cudaStream_t stream);
+int batch_group_max();
+size_t batch_group_state_bytes();  // per space: group barrier + member partials
+int batch_group_max_np();
+size_t batch_job_bytes();
+int batch_group_resident(int num_sms);
+void batch_set_job(void* jobs_host, size_t idx, int item, int member, int g);
+cudaError_t launch_batch_group(const void* descs_dev, const void* jobs_dev, int waves, int grid,
+                               const BatchParams& P, cudaStream_t stream);
 
 // ---- random-walk validator (tk_descent.cu) ------------------------------------
 constexpr int kMaxDescentSlots = 256;

@@ -453,7 +453,7 @@ def test_analysis_pipeline_matches_single_handle(tk):
             assert np.array_equal(a[: w[2]], b)
 
 
-@pytest.mark.parametrize("path", ["batched", "threads"])
+@pytest.mark.parametrize("path", ["batched", "batched_one_cta", "threads"])
 @pytest.mark.parametrize("kind", [O.ADJACENT, O.HAMMING])
 def test_batch_analyzer_matches_oracle(tk, monkeypatch, path, kind):
     """tk.BatchAnalyzer on both of its paths -- one tk_batch_analyze launch with
@@ -463,6 +463,8 @@ def test_batch_analyzer_matches_oracle(tk, monkeypatch, path, kind):
     PageRank within 1e-12."""
     if path == "threads":
         monkeypatch.setenv("TK_BATCH_THREADS", "1")
+    if path == "batched_one_cta":  # one CTA per space (no CTA groups)
+        monkeypatch.setenv("TK_BATCH_NOGROUP", "1")
     shapes = [[8, 6, 3, 3, 2], [12, 6, 8, 8, 2, 2], [4, 4, 3, 3, 3, 3, 4, 4, 2, 2],
               [31, 11, 4, 2, 3], [6, 5, 4, 3, 2, 2, 2], [7, 1, 5], [2, 2]]
     tables = []
