@@ -626,3 +626,38 @@ def test_fused_ffg_build_matches_oracle(tk, monkeypatch, radix, q):
         off, tg, sk, mn = land.ffg_arrays()
     assert np.array_equal(off, ref["offsets"]) and np.array_equal(tg, ref["targets"])
     assert np.array_equal(sk, ref["is_sink"]) and np.array_equal(mn, ref["minima"])
+
+
+def test_batch_analyze_device_inputs_and_long_cp_curve(tk):
+    """tk_batch_analyze with device-resident tables (TK_MEM_DEVICE) and a C_p
+    curve of 31 points (past the CTA-group kernel's partial width: the one-CTA
+    kernel runs), against the oracle."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2210_01465_b200 import _abi
+
+    shapes = [[12, 6, 8, 8, 2, 2], [8, 6, 3, 3, 2], [4, 4, 3, 3, 3, 3, 4, 4, 2, 2]]
+    tables = [O.gen_synthetic(r, 0.3, "rugged", 11 + k) for k, r in enumerate(shapes)]
+    dev = [(torch.from_numpy(np.ascontiguousarray(f)).cuda(), torch.from_numpy(o.astype(np.uint8)).cuda())
+           for f, o in tables]
+    for p_max in (15, 30):
+        arr = (_abi.BatchItem * len(shapes))()
+        for k, r in enumerate(shapes):
+            arr[k].dims = len(r)
+            for i, m in enumerate(r):
+                arr[k].radix[i] = m
+            arr[k].fitness, arr[k].ok = dev[k][0].data_ptr(), dev[k][1].data_ptr()
+        L = _abi.load()
+        assert L.tk_batch_analyze(0, arr, len(shapes), O.ADJACENT, 0.85, 1e-10, 100000, p_max,
+                                  _abi.TK_MEM_DEVICE) == 0
+        for k, r in enumerate(shapes):
+            fit, ok = tables[k]
+            ref = O.analyze(r, fit, ok, O.ADJACENT, p_max_percent=p_max, node_limit=1 << 32)
+            s = arr[k].summary
+            assert arr[k].status == 0
+            assert s.iterations == ref["iterations"] and s.n_cp == p_max + 1
+            assert s.n_minima == len(ref["ffg"]["minima"])
+            for kk, c in ref["c_p_curve"]:
+                assert abs(s.c_p[kk] - c) <= CP_ATOL
