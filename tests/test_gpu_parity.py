@@ -395,6 +395,44 @@ def test_analyze_landscape_matches_oracle(tk, golden):
 
 # ------------------------------------------- full-size, size-independent checks --
 
+@pytest.mark.parametrize("kind", [O.ADJACENT, O.HAMMING])
+@pytest.mark.parametrize("config", ["c1", "c2"])
+def test_baseline_c1_c2_instances_match_oracle(tk, config, kind):
+    """BASELINE.json configs[0] and configs[1] exactly as the bench runs them:
+    C1 = (12,12,12,12) G_iid q = 0 seed 1 generated on the device; C2 =
+    (16,12,8,8,8,4,2,2) generate_synthetic_kernel_space 'rugged' q = 0.3 seed 2
+    (the reference's generator, restated bit-for-bit by the oracle).  FFG CSR
+    and minima bit-exact, PageRank within 1e-12 with the same iteration count,
+    C_p within 1e-9, the report rows exact."""
+    if config == "c1":
+        radix = [12, 12, 12, 12]
+        with tk.Landscape(radix) as src:
+            src.generate(0, 0.0, 1)
+            fit, ok = src.fitness()
+        assert np.array_equal(fit.view(np.uint64), O.gen_iid(O.space_size(radix), 0.0, 1)[0].view(np.uint64))
+    else:
+        radix = [16, 12, 8, 8, 8, 4, 2, 2]
+        fit, ok = O.gen_synthetic(radix, 0.30, "rugged", 2)
+    ref = O.analyze(radix, fit, ok, kind, nthreads=8, node_limit=1 << 32)
+    with tk.Landscape(radix) as land:
+        land.load_dense(fit, ok)
+        s = land.analyze(kind, node_limit=1 << 32, emit_csr=True)
+        off, tg, sk, mn = land.ffg_arrays()
+        r = land.pagerank_vector()
+        rows = land.report_rows(s.f_opt)
+    g = ref["ffg"]
+    assert np.array_equal(off, g["offsets"]) and np.array_equal(tg, g["targets"])
+    assert np.array_equal(sk, g["is_sink"]) and np.array_equal(mn, g["minima"])
+    assert s.iterations == ref["iterations"]
+    assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
+    for k, c in ref["c_p_curve"]:
+        assert abs(s.c_p[k] - c) <= CP_ATOL
+    ranks, fmin, frac, prm = rows
+    assert np.array_equal(ranks, g["minima"].astype(np.uint64))
+    assert np.array_equal(fmin.view(np.uint64), fit[g["minima"]].view(np.uint64))
+    assert np.array_equal(frac, ref["f_opt"] / fit[g["minima"]])
+
+
 @pytest.mark.parametrize("radix,kind,gen,q", [
     ([8, 8, 8, 8, 6, 6, 4, 4, 2, 2], O.ADJACENT, 1, 0.0),   # C3 shape, heavy tails
     ([8, 8, 8, 8, 6, 6, 4, 4, 2, 2], O.HAMMING, 1, 0.0),
