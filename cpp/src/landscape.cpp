@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <memory>
 #include <string>
@@ -235,6 +236,96 @@ DescentReport random_descents(const SearchSpaceCache& cache, NeighbourhoodKind k
     check(tk_descents(land.get(), walkers, seed, restart_scan ? 1 : 0,
                       m ? rep.arrivals.data() : nullptr, &rep.fail_arrivals, &rep.evaluations));
     return rep;
+}
+
+}  // namespace tunekit
+
+namespace tunekit {
+
+std::vector<CentralityReport> analyze_landscapes(const std::vector<const SearchSpaceCache*>& caches,
+                                                 NeighbourhoodKind kind, double damping,
+                                                 int p_max_percent) {
+    const std::size_t n = caches.size();
+    std::vector<CentralityReport> out(n);
+    std::vector<tk_batch_item> items(n);
+    std::vector<std::vector<double>> fit(n);
+    std::vector<std::vector<std::uint8_t>> ok(n);
+    std::vector<std::vector<std::uint64_t>> ranks(n);
+    std::vector<std::vector<double>> fmin(n), frac(n), prv(n);
+    std::vector<bool> batched(n, false);
+    for (std::size_t k = 0; k < n; ++k) {
+        const SearchSpaceCache& c = *caches[k];
+        if (!c.complete())
+            throw Error("landscape analysis needs a complete cache (" +
+                        std::to_string(c.present_count()) + " of " + std::to_string(c.size()) +
+                        " configurations present)");
+        const ParameterSpace& s = c.space();
+        tk_batch_item& it = items[k];
+        std::memset(&it, 0, sizeof(it));
+        std::uint64_t slots = 0;
+        it.dims = static_cast<std::uint32_t>(s.dims());
+        for (std::size_t i = 0; i < s.dims(); ++i) {
+            it.radix[i] = static_cast<std::uint32_t>(s.list_size(i));
+            if (it.radix[i] >= 2) slots += kind == NeighbourhoodKind::Adjacent ? 2 : it.radix[i] - 1;
+        }
+        if (c.size() > 1'000'000) throw InvalidArgument(limit_message(c.size(), 1'000'000));
+        batched[k] = s.dims() <= TK_MAX_DIMS && c.size() <= (1ull << 20) && slots <= 64;
+        if (!batched[k]) continue;
+        fit[k].resize(c.size());
+        ok[k].resize(c.size());
+        for (std::uint64_t r = 0; r < c.size(); ++r) {
+            fit[k][r] = c.mean(r);
+            ok[k][r] = c.ok(r) ? 1 : 0;
+        }
+        // room for every possible minimum: the count is only known afterwards
+        ranks[k].resize(c.size());
+        fmin[k].resize(c.size());
+        frac[k].resize(c.size());
+        prv[k].resize(c.size());
+        it.fitness = fit[k].data();
+        it.ok = ok[k].data();
+        it.minima_ranks = ranks[k].data();
+        it.minima_fitness = fmin[k].data();
+        it.minima_fraction = frac[k].data();
+        it.minima_pagerank = prv[k].data();
+        it.minima_capacity = c.size();
+    }
+    std::vector<tk_batch_item> live;
+    std::vector<std::size_t> idx;
+    for (std::size_t k = 0; k < n; ++k)
+        if (batched[k]) {
+            live.push_back(items[k]);
+            idx.push_back(k);
+        }
+    if (!live.empty())
+        check(tk_batch_analyze(device_index(), live.data(), static_cast<std::uint32_t>(live.size()),
+                               kind_code(kind), damping, 1e-10, 100000, p_max_percent,
+                               TK_MEM_HOST));
+    for (std::size_t j = 0; j < live.size(); ++j) {
+        const std::size_t k = idx[j];
+        const tk_batch_item& it = live[j];
+        const tk_report_summary& s = it.summary;
+        if (it.status != TK_OK) {
+            if (it.status == TK_ENOFEAS) throw NoFeasiblePoint("no feasible point in cache " + std::to_string(k));
+            if (it.status == TK_ENOCONV)
+                throw NonConvergence("pagerank did not converge", static_cast<long>(s.iterations), s.residual);
+            throw Error("proportion_of_centrality: minima hold zero PageRank mass (cache " +
+                        std::to_string(k) + ")");
+        }
+        CentralityReport& rep = out[k];
+        rep.kind = kind;
+        rep.damping = damping;
+        rep.f_opt = s.f_opt;
+        rep.pagerank_iterations = static_cast<int>(s.iterations);
+        rep.pagerank_sum = s.pagerank_sum;
+        for (int p = 0; p < s.n_cp; ++p) rep.c_p_curve.emplace_back(p, s.c_p[p]);
+        rep.minima.reserve(s.n_minima);
+        for (std::uint64_t i = 0; i < s.n_minima; ++i)
+            rep.minima.push_back({ranks[k][i], fmin[k][i], frac[k][i], prv[k][i]});
+    }
+    for (std::size_t k = 0; k < n; ++k)
+        if (!batched[k]) out[k] = analyze_landscape(*caches[k], kind, damping, p_max_percent);
+    return out;
 }
 
 }  // namespace tunekit

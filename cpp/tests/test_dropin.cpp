@@ -3,6 +3,7 @@
 // headers and host classes (cpp/Makefile) -- and dumps every result for
 // tests/test_cpp_dropin.py to compare with the CPU oracle:
 //   test_dropin <outdir> <q> <profile> <seed> <m0> <m1> ...
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -90,6 +91,40 @@ int main(int argc, char** argv) {
                 export_graph(g, cache, f, os);
                 const char* ext = f == GraphFormat::Dot ? "dot" : f == GraphFormat::GraphML ? "graphml" : "csv";
                 std::ofstream(dir + "/graph." + ext) << os.str();
+            }
+        }
+    }
+
+    // analyze_landscapes (extensions.hpp): the batched device path against the
+    // per-space one, for three caches (two spaces)
+    {
+        std::vector<Parameter> ps2;
+        for (int i = 0; i < 4; ++i) {
+            Parameter p;
+            p.name = "q" + std::to_string(i);
+            for (int v = 0; v < 5 + i; ++v) p.values.push_back(std::int64_t{v});
+            ps2.push_back(std::move(p));
+        }
+        const SearchSpaceCache other =
+            generate_synthetic_kernel_space(ParameterSpace(std::move(ps2)), 0.2, prof, seed + 1);
+        const std::vector<const SearchSpaceCache*> cs = {&cache, &other, &cache};
+        for (NeighbourhoodKind kind : {NeighbourhoodKind::Hamming, NeighbourhoodKind::Adjacent}) {
+            const std::vector<CentralityReport> reps = analyze_landscapes(cs, kind);
+            EXPECT(reps.size() == 3);
+            for (std::size_t k = 0; k < cs.size(); ++k) {
+                const CentralityReport one = analyze_landscape(*cs[k], kind);
+                const CentralityReport& b = reps[k];
+                EXPECT(b.pagerank_iterations == one.pagerank_iterations);
+                EXPECT(b.minima.size() == one.minima.size());
+                EXPECT(b.f_opt == one.f_opt);
+                for (std::size_t i = 0; i < b.minima.size() && i < one.minima.size(); ++i) {
+                    EXPECT(b.minima[i].rank == one.minima[i].rank);
+                    EXPECT(b.minima[i].fitness == one.minima[i].fitness);
+                    EXPECT(b.minima[i].fraction_of_optimum == one.minima[i].fraction_of_optimum);
+                    EXPECT(std::abs(b.minima[i].pagerank - one.minima[i].pagerank) <= 1e-12);
+                }
+                for (std::size_t p = 0; p < b.c_p_curve.size(); ++p)
+                    EXPECT(std::abs(b.c_p_curve[p].second - one.c_p_curve[p].second) <= 1e-9);
             }
         }
     }

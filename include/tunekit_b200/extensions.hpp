@@ -26,6 +26,16 @@ CentralityReport analyze_cache_file(const std::string& path, NeighbourhoodKind k
                                     double damping, int p_max_percent, std::uint64_t node_limit,
                                     ParameterSpace* space_out = nullptr);
 
+// analyze_landscape over many caches in one device call (tk_batch_analyze:
+// one upload, one launch with a CTA group per space, one read-back) -- for
+// the 10^3-10^5-configuration spaces of real tuning problems, where the
+// per-space path is bound by launch and synchronisation latency.  Caches of
+// more than 2^20 configurations (or > 64 neighbour slots) are analysed one by
+// one.  Same results and exceptions as analyze_landscape per cache.
+std::vector<CentralityReport> analyze_landscapes(const std::vector<const SearchSpaceCache*>& caches,
+                                                 NeighbourhoodKind kind, double damping = 0.85,
+                                                 int p_max_percent = 15);
+
 // The GPU random-walk validator: `walkers` randomized
 // first-improvement descents -- hillclimb.cpp:48-87 climb_random_first, with a
 // fresh scan order after every move when restart_scan -- from uniform starts,

@@ -56,7 +56,7 @@ def test_dropin_links_the_reference_host_classes(built):
                 "tunekit::proportion_of_centrality", "tunekit::classify_points",
                 "tunekit::minima_fraction_report", "tunekit::export_graph",
                 "tunekit::write_minima_csv", "tunekit::write_cp_curve_csv",
-                "tunekit::random_descents"):
+                "tunekit::random_descents", "tunekit::analyze_landscapes"):
         assert sym in mine, sym
     for sym in ("tunekit::ParameterSpace::rank_of", "tunekit::SearchSpaceCache::finalize",
                 "tunekit::generate_synthetic_kernel_space", "tunekit::load_cache"):
