@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtk_landscape.so")
-SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_rows.cu", "tk_ring.cu",
+SOURCES = ["tk_kernels.cu", "tk_staged.cu", "tk_hamming.cu", "tk_hamsplit.cu", "tk_rows.cu", "tk_ring.cu",
            "tk_descent.cu", "tk_batch.cu", "tk_abi.cu"]
 HEADERS = ["tk_internal.cuh", "tk_kernels.cuh", "tk_pipe.cuh"]
 

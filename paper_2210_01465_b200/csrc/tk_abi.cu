@@ -460,7 +460,12 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                  int smem_budget = 0, int* kernel_used = nullptr, bool ring = false) {
     const int maxg = (plan || rplan) ? num_sms * 4 : tk::pagerank_max_grid(mode, wide, num_sms);
     if (maxg <= 0) return fail(TK_ECUDA, "pagerank: kernel cannot be made resident");
-    TKC(ensure(part, static_cast<size_t>(maxg) * 2 * 3 * 8));
+    // Hamming by dimension groups (tk_hamsplit.cu; TK_HAM_SPLIT=0: the tiled / staged kernels)
+    const char* hs_env = std::getenv("TK_HAM_SPLIT");
+    const bool ham_split = !plan && !rplan && !ring && mode == tk::MODE_HAM && staged_enabled() &&
+                           !(hs_env && hs_env[0] == '0') && tk::ham_split_available(s);
+    TKC(ensure(part, std::max(static_cast<size_t>(maxg) * 2 * 3 * 8,
+                              ham_split ? tk::ham_split_workspace_bytes(s) : size_t{0})));
     const double nd = static_cast<double>(a.n);
     a.inv_n = 1.0 / nd;
     a.nd = nd;
@@ -483,12 +488,14 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
                                      num_sms, (static_cast<uint64_t>(a.n) + plan->T - 1) / plan->T))
                                : num_sms;
     tk::HamStagePlanOut hplan{};
-    const bool ham_staged = !plan && !rplan && mode == tk::MODE_HAM && staged_enabled() &&
+    const bool ham_staged = !ham_split && !plan && !rplan && mode == tk::MODE_HAM && staged_enabled() &&
                             smem_budget > 0 && tk::ham_staged_plan(s, smem_budget, &hplan);
-    const bool ham_tiled = !plan && !ham_staged && mode == tk::MODE_HAM && staged_enabled() &&
+    const bool ham_tiled = !ham_split && !plan && !ham_staged && mode == tk::MODE_HAM && staged_enabled() &&
                            tk::ham_tiled_supported(s);
-    TKC(gated_coop_launch(device, num_sms, (ham_tiled || ham_staged || ring) ? num_sms : footprint, stream, [&] {
+    TKC(gated_coop_launch(device, num_sms, (ham_tiled || ham_staged || ham_split || ring) ? num_sms : footprint, stream, [&] {
         if (ring) return tk::launch_pagerank_ring(s, a, smem_budget, num_sms, &g, stream);
+        if (ham_split)
+            return tk::launch_pagerank_ham_split(s, wide, a, a.r0, part.p, num_sms, &g, stream);
         if (rplan) return tk::launch_pagerank_rows(s, *rplan, a, num_sms, &g, stream);
         if (plan) return tk::launch_pagerank_staged(s, *plan, a, num_sms, &g, stream);
         if (ham_staged)
@@ -497,9 +504,10 @@ int run_pagerank(int device, int num_sms, const tk::DevShape& s, int mode, bool 
         return tk::launch_pagerank(s, mode, wide, a, num_sms, &g, stream);
     }));
     if (e1) TKC(cudaEventRecord(e1, stream));
-    // 0 per-lane, 1 staged (Adjacent), 2 row-tiled, 3 Hamming staged, 4 Hamming tiled, 5 ring
+    // 0 per-lane, 1 staged (Adjacent), 2 row-tiled, 3 Hamming staged, 4 Hamming tiled, 5 ring,
+    // 6 Hamming by dimension groups
     if (kernel_used)
-        *kernel_used = ring ? 5 : rplan ? 2 : plan ? 1 : ham_staged ? 3 : ham_tiled ? 4 : 0;
+        *kernel_used = ring ? 5 : rplan ? 2 : plan ? 1 : ham_split ? 6 : ham_staged ? 3 : ham_tiled ? 4 : 0;
     TKC(cudaMemcpyAsync(&hs->pr, &ds->pr, sizeof(PrOut), cudaMemcpyDeviceToHost, stream));
     TKC(cudaStreamSynchronize(stream));
     if (e0 && e1 && ms) TKC(cudaEventElapsedTime(ms, e0, e1));

@@ -169,6 +169,15 @@ cudaError_t launch_pagerank_ham_staged(const DevShape& s, bool wide, const HamSt
                                        cudaStream_t stream);
 cudaError_t launch_pagerank_ham_tiled(const DevShape& s, bool wide, const PrArgs& a, int num_sms,
                                       int* grid_out, cudaStream_t stream);
+// Hamming: in-edge sum split by dimension groups (tk_hamsplit.cu): one
+// shared-memory window pass per group and iteration, the partial sum carried in
+// r1 / acc1 between passes.  Runs to convergence (host-driven chunks); the
+// result lands in a.r0 like the cooperative kernels'.  ws: at least
+// ham_split_workspace_bytes() of device memory.
+bool ham_split_available(const DevShape& s);
+size_t ham_split_workspace_bytes(const DevShape& s);
+cudaError_t launch_pagerank_ham_split(const DevShape& s, bool wide, const PrArgs& a, double* acc1,
+                                      void* ws, int num_sms, int* grid_out, cudaStream_t stream);
 
 // ---- TMA-staged Adjacent kernels (tk_staged.cu) ------------------------------
 // A tile is T consecutive ranks [v0, v0+T).  The Adjacent neighbours of the tile

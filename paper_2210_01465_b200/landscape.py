@@ -238,7 +238,7 @@ class Landscape:
                                           C.byref(mb), C.byref(mp)))
         return dict(staged_build=bool(sb.value), staged_pagerank=sp.value > 0,
                     pagerank_kernel={1: "staged", 2: "rows", 3: "ham_staged",
-                                     4: "ham_tiled", 5: "ring"}.get(sp.value, "per-lane"),
+                                     4: "ham_tiled", 5: "ring", 6: "ham_split"}.get(sp.value, "per-lane"),
                     pagerank_grid=g.value, ms_build=mb.value, ms_pagerank=mp.value)
 
     # ---- ingestion

@@ -298,9 +298,11 @@ def test_row_tiled_pagerank_matches_oracle(tk, monkeypatch, rows, radix, q):
         assert abs(s.c_p[k] - c) <= CP_ATOL
 
 
-@pytest.mark.parametrize("path", ["staged", "tiled", "v1"])
+@pytest.mark.parametrize("path", ["split", "staged", "tiled", "v1"])
 @pytest.mark.parametrize("radix,q", [
     ([6, 6, 4, 4, 4, 4, 2, 2], 0.2),       # uniform / tile-aligned / per-thread digits
+    ([4, 4, 4, 4, 4, 4, 4, 4, 4, 4], 0.1),  # split: three dimension groups (LO / LOHI / HI / OUTER)
+    ([8, 8, 8, 6, 6, 6, 4, 4, 2], 0.1),    # split: C5's outer dims, three groups
     ([8, 4, 4, 4, 2, 2, 4], 0.0),          # N = 8192, one uniform dim
     ([8, 8, 8, 4, 4, 4, 4, 2, 2], 0.1),    # 35 Hamming slots: u64 in-masks
     ([4, 4, 4, 4, 2], 0.3),                # N = 512: one tile, all digits per thread
@@ -310,10 +312,11 @@ def test_row_tiled_pagerank_matches_oracle(tk, monkeypatch, rows, radix, q):
     ([2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2], 0.1),  # 5 outer binary dims
 ])
 def test_hamming_tiled_pagerank_matches_oracle(tk, monkeypatch, path, radix, q):
-    """The Hamming kernels (tk_hamming.cu: staged -- outer lines through a TMA
-    ring, inner lines from a block copy -- and tiled) and the per-lane one agree
-    with the oracle: same iteration count, rank vector within 1e-12, C_p within
-    1e-9."""
+    """The Hamming kernels (tk_hamsplit.cu: in-edge sum split by dimension
+    groups; tk_hamming.cu: staged -- outer lines through a TMA ring, inner lines
+    from a block copy -- and tiled) and the per-lane one agree with the oracle:
+    same iteration count, rank vector within 1e-12, C_p within 1e-9."""
+    monkeypatch.setenv("TK_HAM_SPLIT", "1" if path == "split" else "0")
     if path == "v1":
         monkeypatch.setenv("TK_KERNELS", "v1")
     if path == "staged":
@@ -329,8 +332,10 @@ def test_hamming_tiled_pagerank_matches_oracle(tk, monkeypatch, path, radix, q):
         f_opt, _ = land.optimum()
         cps = land.centrality(f_opt, [k / 100.0 for k in range(16)])
         used = land.kernel_info()["pagerank_kernel"]
-    if path == "staged" and n > 512:
+    if path == "staged" and n > 512 and radix != [8, 8, 8, 6, 6, 6, 4, 4, 2]:  # strides off 512
         assert used == "ham_staged", used
+    if path == "split" and max(radix) <= 8:
+        assert used == "ham_split", used
     assert it == ref["iterations"]
     assert rel_l1(r, ref["pagerank"]) <= PR_RTOL
     assert abs(s - 1.0) < 1e-9
