@@ -68,7 +68,7 @@ struct SpGroup {
     int threads;          // CTA size
     uint32_t m[kSpMaxGD];
     int off[kSpMaxGD];                   // dim a + k's first slot, relative to base0
-    int dk[kSpMaxGD];                    // window-slot distance between values of dim a + k
+    int dkB[kSpMaxGD];                   // shared-memory bytes between values of dim a + k
     unsigned long long cmagic[kSpMaxGD];  // fdiv by the combo stride of dim a + k
 };
 
@@ -152,21 +152,28 @@ __device__ __forceinline__ void sp_digits(const SpGroup& g, uint32_t c, SpRank& 
     }
 }
 
+__device__ __forceinline__ double sp_lds(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
 // lower in-neighbours of the group's dims, ascending dims and values: the set
-// bits of the dim's lower field (value j at bit j), lowest first
+// bits of the dim's lower field (value j at bit j), lowest first (leading-zero
+// count of the bit-reversed field).  qB: shared address of the rank's slot.
 template <int GD>
-__device__ __forceinline__ double sp_lo(double acc, const double* cs, int q, uint32_t mk,
-                                        const SpGroup& g, const SpRank& r) {
+__device__ __forceinline__ double sp_lo(double acc, uint32_t qB, uint32_t mk, const SpGroup& g,
+                                        const SpRank& r) {
 #pragma unroll
     for (int k = 0; k < GD; ++k) {
         const uint32_t xk = r.x[k];
-        uint32_t f = (mk >> g.off[k]) & ((1u << xk) - 1u);
-        const int dk = g.dk[k];
-        const double* row = cs + q - static_cast<int>(xk) * dk;
-        while (f) {
-            const int j = __ffs(f) - 1;
-            f &= f - 1u;
-            acc = __dadd_rn(acc, row[j * dk]);
+        const uint32_t dkB = static_cast<uint32_t>(g.dkB[k]);
+        uint32_t fr = __brev((mk >> g.off[k]) & ((1u << xk) - 1u));
+        const uint32_t row = qB - xk * dkB;
+        while (fr) {
+            const uint32_t j = __clz(fr);
+            fr &= ~(0x80000000u >> j);
+            acc = __dadd_rn(acc, sp_lds(row + j * dkB));
         }
     }
     return acc;
@@ -175,19 +182,19 @@ __device__ __forceinline__ double sp_lo(double acc, const double* cs, int q, uin
 // upper in-neighbours, descending dims, ascending values (value j > x_k at
 // bit j - 1 of the dim's field)
 template <int GD>
-__device__ __forceinline__ double sp_hi(double acc, const double* cs, int q, uint32_t mk,
-                                        const SpGroup& g, const SpRank& r) {
+__device__ __forceinline__ double sp_hi(double acc, uint32_t qB, uint32_t mk, const SpGroup& g,
+                                        const SpRank& r) {
 #pragma unroll
     for (int kk = 0; kk < GD; ++kk) {
         const int k = GD - 1 - kk;
         const uint32_t xk = r.x[k];
-        uint32_t f = (mk >> (g.off[k] + xk)) & ((1u << (g.m[k] - 1u - xk)) - 1u);
-        const int dk = g.dk[k];
-        const double* row = cs + q + dk;  // value x_k + 1
-        while (f) {
-            const int b = __ffs(f) - 1;
-            f &= f - 1u;
-            acc = __dadd_rn(acc, row[b * dk]);
+        const uint32_t dkB = static_cast<uint32_t>(g.dkB[k]);
+        uint32_t fr = __brev((mk >> (g.off[k] + xk)) & ((1u << (g.m[k] - 1u - xk)) - 1u));
+        const uint32_t row = qB + dkB;  // value x_k + 1
+        while (fr) {
+            const uint32_t b = __clz(fr);
+            fr &= ~(0x80000000u >> b);
+            acc = __dadd_rn(acc, sp_lds(row + b * dkB));
         }
     }
     return acc;
@@ -219,6 +226,8 @@ __global__ void __launch_bounds__(kSpMaxThreads, 2)
     const int nq = static_cast<int>(g.C * g.W);  // ranks per window
     double* cs = sp_smem;                         // c of the window (slot q)
     double* cs2 = sp_smem + nq;                   // OUTER: c' of the window
+    const uint32_t csB = static_cast<uint32_t>(__cvta_generic_to_shared(cs));
+    const uint32_t cs2B = static_cast<uint32_t>(__cvta_generic_to_shared(cs2));
     const int wsh = g.wshift;                     // W = 1 << wsh
     const uint32_t wmask = g.W - 1;
 
@@ -278,8 +287,9 @@ __global__ void __launch_bounds__(kSpMaxThreads, 2)
                 sp_digits<GD>(g, static_cast<uint32_t>(q) >> wsh, r);
                 const uint32_t mk = mkv[si];
                 double acc = accv[si];
-                if (MODE == SP_LO || MODE == SP_LOHI) acc = sp_lo<GD>(acc, cs, q, mk, g, r);
-                if (MODE != SP_LO) acc = sp_hi<GD>(acc, cs, q, mk, g, r);
+                const uint32_t qB = csB + static_cast<uint32_t>(q) * 8u;
+                if (MODE == SP_LO || MODE == SP_LOHI) acc = sp_lo<GD>(acc, qB, mk, g, r);
+                if (MODE != SP_LO) acc = sp_hi<GD>(acc, qB, mk, g, r);
                 const uint32_t v = rank_of(q);
                 if (MODE == SP_LO || MODE == SP_HI || MODE == SP_LOHI) {
                     __stcs(accb + v, acc);
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, 2)
             }
         }
         if (MODE == SP_OUTER || MODE == SP_INIT) {  // lo(g_0) of the next iterate
-            const double* cnew = MODE == SP_OUTER ? cs2 : cs;
+            const uint32_t cnewB = MODE == SP_OUTER ? cs2B : csB;
             if (MODE == SP_OUTER) __syncthreads();
 #pragma unroll
             for (int si = 0; si < kSpNS; ++si) {
@@ -318,7 +328,8 @@ __global__ void __launch_bounds__(kSpMaxThreads, 2)
                 if (q >= nq) continue;
                 SpRank r;
                 sp_digits<GD>(g, static_cast<uint32_t>(q) >> wsh, r);
-                __stcs(accn + rank_of(q), sp_lo<GD>(0.0, cnew, q, mkv[si], g, r));
+                __stcs(accn + rank_of(q),
+                       sp_lo<GD>(0.0, cnewB + static_cast<uint32_t>(q) * 8u, mkv[si], g, r));
             }
         }
         __syncthreads();  // the window's slots are refilled next round
@@ -431,7 +442,7 @@ bool sp_make_group(const DevShape& s, int a, int b, uint32_t W, SpGroup* g) {
         const uint32_t cst = s.stride[a + k] / I;
         t.m[k] = s.radix[a + k];
         t.off[k] = s.base[a + k] - s.base[a];
-        t.dk[k] = static_cast<int>(cst * W);
+        t.dkB[k] = static_cast<int>(cst * W * 8);
         t.cmagic[k] = sp_magic(cst);
     }
     *g = t;
