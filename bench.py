@@ -220,6 +220,29 @@ def kernel_source_sha() -> str:
     return h.hexdigest()[:16]
 
 
+def hamming_traffic(workload: str, iterations: int, kernel: str):
+    """DRAM bytes (read + write) of one Hamming PageRank (all dimension-group
+    passes) from the committed ncu launch list (profiles/hamming_traffic.json),
+    used only for the same workload, iteration count and tk_hamsplit.cu source;
+    (None, why) otherwise."""
+    import hashlib
+
+    if kernel != "ham_split":
+        return None, f"capture taken on the ham_split kernel, not {kernel}"
+    try:
+        with open(os.path.join(ROOT, "profiles", "hamming_traffic.json")) as f:
+            t = json.load(f)
+        with open(os.path.join(ROOT, "paper_2210_01465_b200", "csrc", "tk_hamsplit.cu"), "rb") as f:
+            sha = hashlib.sha256(f.read()).hexdigest()[:16]
+    except (OSError, ValueError):
+        return None, "no committed capture"
+    if (t.get("workload"), t.get("iterations")) != (workload, iterations):
+        return None, "capture taken on another workload"
+    if t.get("kernel_source_sha") != sha:
+        return None, f"capture taken on kernel source {t.get('kernel_source_sha')}, not this one"
+    return t["dram_bytes_per_pagerank"], t.get("source", "")
+
+
 def measured_traffic(workload: str, kind: str, iterations: int):
     """DRAM bytes (read + write) per PageRank launch from the committed ncu
     --set full capture (profiles/pagerank_traffic.json, scripts/
@@ -529,7 +552,11 @@ def run_b200(args, wl, kind):
                             "bytes_model": "25 B/node/iteration: u64 in-mask 8 + outdeg 1 + c "
                                            "read once 8 + c' 8; + 33 B/node prologue and "
                                            "closing pass",
-                            "algorithmic_bytes_per_launch": hbytes}}
+                            "algorithmic_bytes_per_launch": hbytes,
+                            "traffic": None}}
+        ht, hsrc = hamming_traffic(args.workload, hit, land.kernel_info()["pagerank_kernel"])
+        ham["roofline"]["traffic"] = ht
+        ham["roofline"]["traffic_source"] = hsrc
 
     # ---- e2e: the same analysis from pinned host buffers through the public API.
     # tk.AnalysisPipeline double-buffers two device handles: every step uploads its
