@@ -60,6 +60,8 @@ VARIANTS = {
     "p6": ["-DTK_PROD_WARPS=6"],
     "pw3": ["-DTK_PW_AHEAD=3"],
     "hm1": ["-DTK_HAM_MINB=1"],
+    "sp3": ["-DTK_SP_MINB=3"],  # Hamming dimension-group passes: 3 CTAs per SM (42 registers)
+    "sp1": ["-DTK_SP_MINB=1"],
     "hu4": ["-DTK_HAM_UNROLL=4"],
     "pw4": ["-DTK_PW_AHEAD=4"],
     "s3": ["-DTK_MAX_STAGES=3"],  # at most 3 pipeline stages (more L1 left)

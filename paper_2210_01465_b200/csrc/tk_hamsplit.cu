@@ -54,6 +54,10 @@ constexpr int kSpChunk = 4;       // iterations enqueued per host round trip
 constexpr int kSpMaxPartCtas = 4096;
 constexpr uint32_t kSpMinW = 8;   // outer windows: >= 64-byte runs per line value
 
+#ifndef TK_SP_MINB
+#define TK_SP_MINB 2  // CTAs per SM the register budget is sized for
+#endif
+
 enum SpMode : int { SP_LO = 0, SP_HI = 1, SP_LOHI = 2, SP_OUTER = 3, SP_INIT = 4, SP_FINAL = 5 };
 
 struct SpGroup {
@@ -201,7 +205,7 @@ __device__ __forceinline__ double sp_hi(double acc, uint32_t qB, uint32_t mk, co
 }
 
 template <int GD, int MODE, typename MW>
-__global__ void __launch_bounds__(kSpMaxThreads, 2)
+__global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
     ham_split_kernel(const SpGroup g, const SpArgs a) {
     extern __shared__ double sp_smem[];
     __shared__ double s_red[kSpMaxThreads / 32];
