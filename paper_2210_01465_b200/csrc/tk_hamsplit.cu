@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
     SpState* st = a.st;
     if (MODE != SP_INIT && MODE != SP_FINAL && st->done) return;  // converged: queued passes exit
     const int tid = threadIdx.x;
-    const int T = blockDim.x;
+    constexpr int T = kSpMaxThreads;  // every pass runs 512-thread CTAs
     if (MODE == SP_OUTER || MODE == SP_INIT)
         if (tid <= kSpMaxDeg) s_rcp[tid] = tid ? __drcp_rn(tid) : 0.0;
     const long long it = st->it;
@@ -239,8 +239,15 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
     for (uint32_t widx = blockIdx.x; widx < g.nwin; widx += gridDim.x) {
         const uint32_t o = widx / g.ipw, ib = widx - o * g.ipw;
         const uint32_t vbase = o * g.C * g.I + ib * g.W;
-        auto rank_of = [&](int q) -> uint32_t {
-            return vbase + (static_cast<uint32_t>(q) >> wsh) * g.I + (static_cast<uint32_t>(q) & wmask);
+        // slot q = tid + si * T: W divides T, so the rank advances by a fixed
+        // stride per si and the inner offset is the thread's own
+        const uint32_t v_t = vbase + (static_cast<uint32_t>(tid) >> wsh) * g.I +
+                             (static_cast<uint32_t>(tid) & wmask);
+        const uint32_t v_step = (static_cast<uint32_t>(T) >> wsh) * g.I;
+        auto rank_of = [&](int si) -> uint32_t {  // recomputed at each use (no hoisted addresses)
+            uint32_t st = v_step;
+            asm volatile("" : "+r"(st));
+            return v_t + static_cast<uint32_t>(si) * st;
         };
         // every global load of the window at once: c straight into shared memory
         // (cp.async), the partial sums, in-mask fields and out-degrees into registers
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
             accv[si] = 0.0;
             mkv[si] = 0u;
             if (q < nq) {
-                const uint32_t v = rank_of(q);
+                const uint32_t v = rank_of(si);
                 if (MODE != SP_INIT) sp_cp8(cs + q, cc + v);
                 mkv[si] = sp_mask<MW>(a.inm, v, g.base0);
                 if (MODE != SP_INIT) accv[si] = __ldcs(accb + v);
@@ -275,7 +282,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
                     cv = a.inv_n;
                     ldang = __dadd_rn(ldang, a.inv_n);
                 }
-                __stcg(cn + rank_of(q), cv);
+                __stcg(cn + rank_of(si), cv);
                 cs[q] = cv;
             }
         } else {
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
                 const uint32_t qB = csB + static_cast<uint32_t>(q) * 8u;
                 if (MODE == SP_LO || MODE == SP_LOHI) acc = sp_lo<GD>(acc, qB, mk, g, r);
                 if (MODE != SP_LO) acc = sp_hi<GD>(acc, qB, mk, g, r);
-                const uint32_t v = rank_of(q);
+                const uint32_t v = rank_of(si);
                 if (MODE == SP_LO || MODE == SP_HI || MODE == SP_LOHI) {
                     __stcs(accb + v, acc);
                     continue;
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(kSpMaxThreads, TK_SP_MINB)
                 if (q >= nq) continue;
                 SpRank r;
                 sp_digits<GD>(g, static_cast<uint32_t>(q) >> wsh, r);
-                __stcs(accn + rank_of(q),
+                __stcs(accn + rank_of(si),
                        sp_lo<GD>(0.0, cnewB + static_cast<uint32_t>(q) * 8u, mkv[si], g, r));
             }
         }
@@ -439,9 +446,8 @@ bool sp_make_group(const DevShape& s, int a, int b, uint32_t W, SpGroup* g) {
     t.nwin = static_cast<uint32_t>(static_cast<uint64_t>(s.n) / (C * W));
     t.ipw = I / W;
     t.base0 = s.base[a];
-    const uint32_t nq = static_cast<uint32_t>(C * W);
-    const uint32_t rounds = (nq + kSpMaxThreads - 1) / kSpMaxThreads;
-    t.threads = static_cast<int>(((nq + rounds - 1) / rounds + 31) / 32 * 32);
+    if (kSpMaxThreads % W) return false;
+    t.threads = kSpMaxThreads;
     for (int k = 0; k < t.gd; ++k) {
         const uint32_t cst = s.stride[a + k] / I;
         t.m[k] = s.radix[a + k];
