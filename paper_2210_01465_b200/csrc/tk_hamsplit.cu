@@ -162,6 +162,20 @@ __device__ __forceinline__ double sp_lds(uint32_t addr) {
     return v;
 }
 
+// acc += the values at row + j * dkB for the set bits j of the field, lowest
+// first; fr is the bit-reversed field, so its highest set bit (bfind: position
+// p) is j = 31 - p, at address row + 31 dkB - p dkB
+__device__ __forceinline__ double sp_walk(double acc, uint32_t fr, uint32_t row, uint32_t dkB) {
+    const uint32_t top = row + 31u * dkB;
+    while (fr) {
+        uint32_t pos;
+        asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(fr));
+        fr ^= 1u << pos;
+        acc = __dadd_rn(acc, sp_lds(top - pos * dkB));
+    }
+    return acc;
+}
+
 // lower in-neighbours of the group's dims, ascending dims and values: the set
 // bits of the dim's lower field (value j at bit j), lowest first (leading-zero
 // count of the bit-reversed field).  qB: shared address of the rank's slot.
@@ -172,13 +186,8 @@ __device__ __forceinline__ double sp_lo(double acc, uint32_t qB, uint32_t mk, co
     for (int k = 0; k < GD; ++k) {
         const uint32_t xk = r.x[k];
         const uint32_t dkB = static_cast<uint32_t>(g.dkB[k]);
-        uint32_t fr = __brev((mk >> g.off[k]) & ((1u << xk) - 1u));
-        const uint32_t row = qB - xk * dkB;
-        while (fr) {
-            const uint32_t j = __clz(fr);
-            fr &= ~(0x80000000u >> j);
-            acc = __dadd_rn(acc, sp_lds(row + j * dkB));
-        }
+        const uint32_t fr = __brev((mk >> g.off[k]) & ((1u << xk) - 1u));
+        acc = sp_walk(acc, fr, qB - xk * dkB, dkB);
     }
     return acc;
 }
@@ -193,13 +202,8 @@ __device__ __forceinline__ double sp_hi(double acc, uint32_t qB, uint32_t mk, co
         const int k = GD - 1 - kk;
         const uint32_t xk = r.x[k];
         const uint32_t dkB = static_cast<uint32_t>(g.dkB[k]);
-        uint32_t fr = __brev((mk >> (g.off[k] + xk)) & ((1u << (g.m[k] - 1u - xk)) - 1u));
-        const uint32_t row = qB + dkB;  // value x_k + 1
-        while (fr) {
-            const uint32_t b = __clz(fr);
-            fr &= ~(0x80000000u >> b);
-            acc = __dadd_rn(acc, sp_lds(row + b * dkB));
-        }
+        const uint32_t fr = __brev((mk >> (g.off[k] + xk)) & ((1u << (g.m[k] - 1u - xk)) - 1u));
+        acc = sp_walk(acc, fr, qB + dkB, dkB);  // value x_k + 1 at bit 0
     }
     return acc;
 }
